@@ -1,0 +1,177 @@
+/* chem.h — C ABI of libchem.so: bulk-sparse stiff chemistry integration on B200 (sm_100a).
+ *
+ * The operation (§2.1): every cell i is an independent constant-volume,
+ * ideal-gas 0-D reactor ("each cell in the domain simulates a 0D reactor, assuming constant volume
+ * and the ideal gas law") integrated over the flow step [0, dt] ("0 < t_i < dt_CFL"):
+ *      dY_k/dt = W_k Omega_k / rho                                     (Eq. 5)
+ *      dT/dt   = - sum_k eps_k Omega_k / (rho sum_k Y_k c_v,k)          (Eq. 6, corrected
+ *                                                                         reading)
+ * with Omega_k from the matrix-based rate formulation (BASELINE.json north_star; SURVEY.md §8(a)
+ * A4), T recovered by Newton-Raphson at constant (e, rho), the gate of Alg. 2/3
+ * (T < T_min or solid -> untouched) and the bulk-sparse schedule of
+ * Alg. 3: count -> bulk bursts of <= K_max substeps while N_active > N* -> compact to a
+ * cell index map -> sparse integration with K_max = 1e5.  One launch per phase
+ * spans every box ("a single kernel across all cells from all grids").
+ *
+ * Conventions for every entry point:
+ *  - Array pointers are DEVICE pointers owned by the caller unless stated otherwise.
+ *  - Layout is component-major ("column-major", Alg. 1): component c of cell i
+ *    is at p[c*ld + i], ld >= n.  Species order is the mechanism's.
+ *  - SI units: rho kg/m^3, e J/kg (mass-specific internal energy), T K, t s, Omega mol/(m^3 s).
+ *  - All device work is enqueued on `stream` (a cudaStream_t, NULL = legacy default stream).
+ *  - Return 0 on success or a negative CHEM_E* code; text via chem_strerror().  Per-cell
+ *    problems (non-convergence, non-finite state) are NOT call errors: they are counted in
+ *    chem_stats.  The library never aborts the process.
+ *  - A chem_ctx is bound to one device; it is not re-entrant (one host thread at a time).
+ */
+#ifndef CHEM_H
+#define CHEM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- error codes ---------------------------------------------------------------------- */
+#define CHEM_OK 0
+#define CHEM_EINVAL (-1)      /* null pointer, n < 0, ld < n, dt <= 0, rtol <= 0, bad option   */
+#define CHEM_EMECH (-2)       /* mechanism tables fail validation (mass/element balance > 1e-10
+                                 relative, W <= 0, non-contiguous T ranges, unknown type)        */
+#define CHEM_ENOSTRUCT (-3)   /* valid mechanism whose reaction structure is not compiled in    */
+#define CHEM_ECUDA (-4)       /* CUDA runtime error (sticky for the ctx); see chem_strerror     */
+#define CHEM_ENOWS (-5)       /* workspace too small (see chem_workspace_bytes)                 */
+
+/* ---- mechanism tables (HOST pointers; copied by chem_init, caller may free afterwards) --- */
+#define CHEM_RXN_ELEMENTARY 0
+#define CHEM_RXN_THREE_BODY 1
+#define CHEM_RXN_LINDEMANN 2
+#define CHEM_RXN_TROE 3
+
+typedef struct {
+    int32_t ns, nr, ne;        /* species (<= 32), reaction rows, elements                     */
+    const double* W;           /* [ns] molar masses, kg/mol                                    */
+    const double* nasa_lo;     /* [ns][7] NASA-7 coefficients for T in [T_lo, T_mid]           */
+    const double* nasa_hi;     /* [ns][7] NASA-7 coefficients for T in [T_mid, T_hi]           */
+    const double* T_range;     /* [ns][3] T_lo, T_mid, T_hi                                    */
+    const int32_t* elem;       /* [ns][ne] atom counts (validation)                            */
+    const double* nu_f;        /* [nr][ns] reactant stoichiometric coefficients nu'            */
+    const double* nu_r;        /* [nr][ns] product stoichiometric coefficients nu''            */
+    const double* A;           /* [nr] pre-exponential (k_inf for falloff rows), SI-molar      */
+    const double* b;           /* [nr] temperature exponent                                    */
+    const double* Ea;          /* [nr] activation energy, J/mol                                */
+    const int32_t* type;       /* [nr] CHEM_RXN_*                                              */
+    const int32_t* reversible; /* [nr] 1: reverse rate from K_c (NASA Gibbs, p_ref)            */
+    const double* eff;         /* [nr][ns] third-body efficiencies (1 = default)               */
+    const double* A0;          /* [nr] falloff low-pressure limit k_0 (k_0 multiplies [M])     */
+    const double* b0;          /* [nr]                                                          */
+    const double* Ea0;         /* [nr] J/mol                                                    */
+    const double* troe;        /* [nr][4] alpha, T***, T*, T** (T** <= 0: term absent)          */
+    double R;                  /* gas constant, 8.314462618 J/(mol K)                           */
+    double p_ref;              /* standard pressure of K_c, 101325 Pa                           */
+} chem_mech_desc;
+
+/* ---- options ------------------------------------------------------------------------------ */
+#define CHEM_METHOD_RODAS4 0   /* 6-stage order-4 L-stable Rosenbrock, embedded order 3 (default) */
+#define CHEM_METHOD_RODAS3 1   /* 4-stage order-3 L-stable Rosenbrock, embedded order 2           */
+
+typedef struct {
+    double T_min;           /* gate T_reaction_min (value unstated -> 500 K) */
+    int32_t kmax_bulk;      /* attempted substeps per cell per bulk launch (K_max = 5)     */
+    int64_t n_active_star;  /* bulk->sparse threshold N*_active (1e4)               */
+    int32_t kmax_sparse;    /* attempted substeps in the sparse launch (1e5)              */
+    double atol_T;          /* absolute tolerance on the integrated temperature, K               */
+    int32_t method;         /* CHEM_METHOD_*                                                      */
+    int32_t compact_bulk;   /* 1 (default): bulk bursts run over the compacted active list;
+                               0: every bulk launch spans all cells of all boxes (paper's Alg. 3) */
+} chem_opts;
+
+/* fills the paper's defaults: 500 K, 5, 1e4, 1e5, 1e-6 K, RODAS4, compact_bulk = 1 */
+void chem_default_opts(chem_opts* o);
+
+/* ---- one AMR box / grid (FAB analogue) for the fused multi-box call ----------------- */
+typedef struct {
+    const double* rho;      /* [ncells]        device                                           */
+    const double* e;        /* [ncells]        device, mass-specific internal energy            */
+    double* T;              /* [ncells]        device, in: gate + Newton guess; out: T(e, Y_out) */
+    double* Y;              /* [ns][ld]        device, in/out                                   */
+    const uint8_t* solid;   /* [ncells] or NULL device; nonzero = embedded solid (not integrated)*/
+    int64_t ncells, ld;
+    double dt;              /* t_final of this box (AMR subcycling: each level its own dt) */
+} chem_box;
+
+/* ---- statistics (host struct filled at the end of a call) ---------------------------------- */
+typedef struct {
+    int64_t cells;              /* cells in the call                                           */
+    int64_t active0;            /* N_active after the gate (Alg. 3 §1)                          */
+    int64_t bulk_iters;         /* bulk launches (Alg. 3 §2 loop trips)                         */
+    int64_t sparse_cells;       /* cells handed to the sparse launch (Alg. 3 §3)                */
+    int64_t steps_attempted;    /* substeps attempted (accepted + rejected), all cells          */
+    int64_t steps_accepted;
+    int64_t rhs_evals, jac_evals, lu_count;
+    int64_t n_unfinished;       /* cells with t < dt after the sparse launch (K_max exceeded)   */
+    int64_t n_newton_fail;      /* temperature Newton not converged in 50 iterations            */
+    int64_t n_nonfinite;        /* non-finite state / step size underflow                       */
+    int64_t n_T_range;          /* finished cells whose T lies outside the NASA ranges          */
+    double t_gate_ms, t_bulk_ms, t_compact_ms, t_sparse_ms;   /* CUDA-event phase times         */
+    double max_energy_drift;    /* max |T_int - T(e, Y_out)| / T over finished cells            */
+    int64_t active_per_iter[16];/* N_active after each of the first 16 bulk launches (App. B)   */
+} chem_stats;
+
+typedef struct chem_ctx chem_ctx;   /* opaque, library-owned */
+
+/* Validate the tables, match their reaction structure against the
+ * compiled structures, copy the numbers for the kernels.  `opts` may be NULL (defaults).
+ * device = CUDA ordinal the ctx is bound to.  On success *out is a new ctx. */
+int chem_init(const chem_mech_desc* mech, const chem_opts* opts, int device, chem_ctx** out);
+void chem_finalize(chem_ctx* ctx);
+const char* chem_strerror(int code);
+/* name of the compiled structure the ctx runs on, or "" */
+const char* chem_structure_name(const chem_ctx* ctx);
+int chem_set_opts(chem_ctx* ctx, const chem_opts* opts);
+
+/* Device workspace (bytes, 256-aligned pointer) a chem_integrate* call needs for up to
+ * max_cells cells in up to max_boxes boxes.  Owned by the caller (e.g. torch.empty). */
+size_t chem_workspace_bytes(const chem_ctx* ctx, int64_t max_cells, int32_t max_boxes);
+
+/* Molar production rates Omega.  wdot is [ns][ld].  Never synchronises. */
+int chem_rates(chem_ctx* ctx, int64_t n, int64_t ld, const double* rho, const double* T,
+               const double* Y, double* wdot, void* stream);
+
+/* Integrate n cells of one box over [0, dt] (the single-box form of chem_integrate_boxes).
+ * T: in = gate temperature and Newton guess, out = T(e, Y_out).  Y in/out.  solid nullable.
+ * rtol, atol: tolerances of the error-controlled integrator on Y_k (atol_T from opts on T).
+ * stats (HOST, nullable).  Synchronises `stream` to read the bulk-loop counters (as the paper
+ * does) and once at the end. */
+int chem_integrate(chem_ctx* ctx, int64_t n, int64_t ld, const double* rho, const double* e,
+                   double* T, double* Y, const uint8_t* solid, double dt, double rtol, double atol,
+                   void* ws, size_t ws_bytes, chem_stats* stats, void* stream);
+
+/* The fused multi-box call: `boxes` is a HOST array of nboxes descriptors.  One launch per
+ * phase spans all boxes through a cell index map.  box_cost (DEVICE, [nboxes],
+ * nullable) receives the attempted substeps summed over each box's cells: the per-box
+ * chemistry cost used for load balancing. */
+int chem_integrate_boxes(chem_ctx* ctx, int32_t nboxes, const chem_box* boxes, double rtol,
+                         double atol, void* ws, size_t ws_bytes, double* box_cost,
+                         chem_stats* stats, void* stream);
+
+/* Test hooks and caller-side helpers ------------------------------------------------------ */
+/* T = Newton(e, Y) seeded with the incoming T.  T in/out [n]. */
+int chem_temperature(chem_ctx* ctx, int64_t n, int64_t ld, const double* e, const double* Y,
+                     double* T, void* stream);
+/* e = u(T, Y) = sum_k Y_k eps_k(T)/W_k (the inverse of chem_temperature). */
+int chem_energy(chem_ctx* ctx, int64_t n, int64_t ld, const double* T, const double* Y, double* e,
+                void* stream);
+/* Analytic Jacobian of the ODE right-hand side w.r.t. y = (Y_1..Y_ns, T), n_unk = ns + 1:
+ * J[(i*n_unk + j)*ld + cell] = d f_i / d y_j (rows of inert species are zero). */
+int chem_jacobian(chem_ctx* ctx, int64_t n, int64_t ld, const double* rho, const double* T,
+                  const double* Y, double* J, void* stream);
+/* ODE right-hand side f = dy/dt, f[(i)*ld + cell], i < ns + 1 (Eq. 5 and corrected Eq. 6). */
+int chem_rhs(chem_ctx* ctx, int64_t n, int64_t ld, const double* rho, const double* T,
+             const double* Y, double* f, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CHEM_H */

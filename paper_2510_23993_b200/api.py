@@ -1,0 +1,211 @@
+"""Torch-facing API over the C ABI (same names as include/chem.h).
+
+PyTorch provides device memory and the current CUDA stream; every computation happens in
+libchem.so.  Arrays follow the C ABI layout: per-cell scalars are 1-D float64 CUDA tensors of
+length >= n, species arrays are [ns, ld] float64 CUDA tensors (component-major).
+"""
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+
+import torch
+
+from . import binding as _b
+from . import mechanism as _mech
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def _check(t, name, dtype=torch.float64):
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor (there is no CPU path)")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}")
+
+
+def _species(Y, ns):
+    _check(Y, "Y")
+    if Y.dim() != 2 or Y.shape[0] != ns or Y.stride(1) != 1:
+        raise ValueError(f"Y must be [ns={ns}, ld] with unit stride along cells")
+    return Y.stride(0)
+
+
+@dataclasses.dataclass
+class Box:
+    """One AMR box (FAB analogue): views into caller tensors, integrated in place."""
+    rho: torch.Tensor
+    e: torch.Tensor
+    T: torch.Tensor
+    Y: torch.Tensor          # [ns, ld]
+    dt: float
+    solid: torch.Tensor | None = None
+
+    @property
+    def ncells(self):
+        return self.rho.shape[0]
+
+
+class Chem:
+    """A chem_ctx bound to one mechanism and one CUDA device."""
+
+    def __init__(self, mech="h2air_li2004", device=None, **opts):
+        self.lib = _b.load_library()
+        self.mech = mech if isinstance(mech, _mech.MechTables) else _mech.load(mech)
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        self.ns = self.mech.ns
+        desc, self._keep = _b.mech_desc(self.mech)
+        self.opts = _b.default_opts(self.lib)
+        for k, v in opts.items():
+            setattr(self.opts, k, v)
+        h = ctypes.c_void_p()
+        rc = self.lib.chem_init(ctypes.byref(desc), ctypes.byref(self.opts), self.device.index, ctypes.byref(h))
+        if rc != 0:
+            raise _b.ChemError(rc, self.lib)
+        self._h = h
+        self._ws = None
+        self.last_stats = None
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            self.lib.chem_finalize(h)
+            self._h = None
+
+    @property
+    def structure(self) -> str:
+        return self.lib.chem_structure_name(self._h).decode()
+
+    def set_opts(self, **opts):
+        for k, v in opts.items():
+            setattr(self.opts, k, v)
+        rc = self.lib.chem_set_opts(self._h, ctypes.byref(self.opts))
+        if rc != 0:
+            raise _b.ChemError(rc, self.lib)
+
+    def _stream(self):
+        return ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def _call(self, rc):
+        if rc != 0:
+            raise _b.ChemError(rc, self.lib)
+
+    def workspace(self, max_cells, max_boxes=1):
+        nbytes = self.lib.chem_workspace_bytes(self._h, int(max_cells), int(max_boxes))
+        if self._ws is None or self._ws.numel() < nbytes:
+            self._ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=self.device)
+        return self._ws
+
+    # ---- point evaluations ---------------------------------------------------------------
+    def rates(self, rho, T, Y, out=None):
+        n = rho.shape[0]
+        ld = _species(Y, self.ns)
+        _check(rho, "rho"); _check(T, "T")
+        if out is None:
+            out = torch.empty((self.ns, ld), dtype=torch.float64, device=self.device)
+        self._call(self.lib.chem_rates(self._h, n, ld, _ptr(rho), _ptr(T), _ptr(Y), _ptr(out), self._stream()))
+        return out
+
+    def rhs(self, rho, T, Y, out=None):
+        n = rho.shape[0]
+        ld = _species(Y, self.ns)
+        if out is None:
+            out = torch.empty((self.ns + 1, ld), dtype=torch.float64, device=self.device)
+        self._call(self.lib.chem_rhs(self._h, n, ld, _ptr(rho), _ptr(T), _ptr(Y), _ptr(out), self._stream()))
+        return out
+
+    def jacobian(self, rho, T, Y):
+        n = rho.shape[0]
+        ld = _species(Y, self.ns)
+        nn = self.ns + 1
+        J = torch.empty((nn * nn, ld), dtype=torch.float64, device=self.device)
+        self._call(self.lib.chem_jacobian(self._h, n, ld, _ptr(rho), _ptr(T), _ptr(Y), _ptr(J), self._stream()))
+        return J.view(nn, nn, ld)
+
+    def temperature(self, e, Y, T):
+        """In place: T <- Newton(e, Y) seeded with T."""
+        n = e.shape[0]
+        ld = _species(Y, self.ns)
+        self._call(self.lib.chem_temperature(self._h, n, ld, _ptr(e), _ptr(Y), _ptr(T), self._stream()))
+        return T
+
+    def energy(self, T, Y, out=None):
+        n = T.shape[0]
+        ld = _species(Y, self.ns)
+        if out is None:
+            out = torch.empty(n, dtype=torch.float64, device=self.device)
+        self._call(self.lib.chem_energy(self._h, n, ld, _ptr(T), _ptr(Y), _ptr(out), self._stream()))
+        return out
+
+    # ---- integration ------------------------------------------------------------------------
+    def integrate(self, rho, e, T, Y, dt, rtol=1e-9, atol=1e-20, solid=None):
+        """In place on T and Y (chem_integrate).  Returns the chem_stats dict."""
+        n = rho.shape[0]
+        ld = _species(Y, self.ns)
+        for t, nm in ((rho, "rho"), (e, "e"), (T, "T")):
+            _check(t, nm)
+        if solid is not None:
+            _check(solid, "solid", torch.uint8)
+        ws = self.workspace(n, 1)
+        st = _b.ChemStats()
+        self._call(self.lib.chem_integrate(self._h, n, ld, _ptr(rho), _ptr(e), _ptr(T), _ptr(Y), _ptr(solid),
+                                           float(dt), float(rtol), float(atol), _ptr(ws), ws.numel(),
+                                           ctypes.byref(st), self._stream()))
+        self.last_stats = st.to_dict()
+        return self.last_stats
+
+    def integrate_boxes(self, boxes, rtol=1e-9, atol=1e-20, box_cost=None):
+        """Fused multi-box call (chem_integrate_boxes).  box_cost: optional float64 CUDA [nboxes]."""
+        nb = len(boxes)
+        arr = (_b.ChemBox * nb)()
+        total = 0
+        for i, bx in enumerate(boxes):
+            ld = _species(bx.Y, self.ns)
+            arr[i].rho = bx.rho.data_ptr()
+            arr[i].e = bx.e.data_ptr()
+            arr[i].T = bx.T.data_ptr()
+            arr[i].Y = bx.Y.data_ptr()
+            arr[i].solid = bx.solid.data_ptr() if bx.solid is not None else None
+            arr[i].ncells = bx.ncells
+            arr[i].ld = ld
+            arr[i].dt = float(bx.dt)
+            total += bx.ncells
+        ws = self.workspace(total, nb)
+        if box_cost is not None:
+            _check(box_cost, "box_cost")
+        st = _b.ChemStats()
+        self._call(self.lib.chem_integrate_boxes(self._h, nb, arr, float(rtol), float(atol), _ptr(ws), ws.numel(),
+                                                 _ptr(box_cost), ctypes.byref(st), self._stream()))
+        self.last_stats = st.to_dict()
+        return self.last_stats
+
+
+class HostRunner:
+    """End-to-end public-API path for host-resident data (the bench's `e2e` leg): pinned host
+    buffers -> H2D copies on the current stream -> chem_integrate_boxes -> D2H of (T, Y)."""
+
+    def __init__(self, chem: Chem, host_boxes):
+        self.chem = chem
+        self.host = host_boxes          # list of dict(rho, e, T, Y, dt) pinned CPU tensors
+        dev = chem.device
+        self.dev_boxes = [Box(torch.empty_like(h["rho"], device=dev), torch.empty_like(h["e"], device=dev),
+                              torch.empty_like(h["T"], device=dev), torch.empty_like(h["Y"], device=dev), h["dt"])
+                          for h in host_boxes]
+        self.out_T = [torch.empty_like(h["T"]).pin_memory() for h in host_boxes]
+        self.out_Y = [torch.empty_like(h["Y"]).pin_memory() for h in host_boxes]
+        self.h2d_bytes = sum(sum(h[k].numel() * 8 for k in ("rho", "e", "T", "Y")) for h in host_boxes)
+        self.d2h_bytes = sum(h["T"].numel() * 8 + h["Y"].numel() * 8 for h in host_boxes)
+
+    def step(self, rtol, atol):
+        for h, d in zip(self.host, self.dev_boxes):
+            d.rho.copy_(h["rho"], non_blocking=True)
+            d.e.copy_(h["e"], non_blocking=True)
+            d.T.copy_(h["T"], non_blocking=True)
+            d.Y.copy_(h["Y"], non_blocking=True)
+        st = self.chem.integrate_boxes(self.dev_boxes, rtol=rtol, atol=atol)
+        for d, oT, oY in zip(self.dev_boxes, self.out_T, self.out_Y):
+            oT.copy_(d.T, non_blocking=True)
+            oY.copy_(d.Y, non_blocking=True)
+        return st

@@ -1,0 +1,650 @@
+// chem_api.cu — the C ABI of include/chem.h: validation, structure matching, workspace, and the
+// host side of the bulk-sparse schedule (Alg. 3).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "../../include/chem.h"
+#include "chem_kernels.cuh"
+
+using namespace chem;
+
+namespace {
+
+constexpr int kIntegrateBS = 64;   // threads per block of k_integrate (per-thread smem ~0.7 KB)
+constexpr int kStreamBS = 256;     // gate / compaction / box cost
+constexpr int kPointBS = 128;      // point kernels
+
+// ------------------------------------------------------------------ per-structure operations
+struct Ops {
+    const char* name;
+    int ns, nr, nsa;
+    size_t params_size;
+    bool (*match)(const chem_mech_desc*);
+    void (*fill)(const chem_mech_desc*, void*);
+    cudaError_t (*rates)(const void*, int64_t, int64_t, const double*, const double*, const double*, double*,
+                         cudaStream_t);
+    cudaError_t (*rhs)(const void*, int64_t, int64_t, const double*, const double*, const double*, double*,
+                       cudaStream_t);
+    cudaError_t (*jacobian)(const void*, int64_t, int64_t, const double*, const double*, const double*, double*,
+                            cudaStream_t);
+    cudaError_t (*temperature)(const void*, int64_t, int64_t, const double*, const double*, double*,
+                               unsigned long long*, cudaStream_t);
+    cudaError_t (*energy)(const void*, int64_t, int64_t, const double*, const double*, double*, cudaStream_t);
+    cudaError_t (*integrate)(const void*, int method, const LaunchCtx&, const uint32_t*, int64_t, int, int, int,
+                             int grid, cudaStream_t);
+    int (*blocks_per_sm)(int method);
+    size_t integrate_smem;
+};
+
+inline int grid_for(int64_t n, int bs, int cap = 148 * 32)
+{
+    const int64_t g = (n + bs - 1) / bs;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(g, cap));
+}
+
+template <class M>
+struct MechOps {
+    using P = Params<M>;
+
+    static bool match(const chem_mech_desc* d)
+    {
+        if (d->ns != M::NS || d->nr != M::NR) return false;
+        for (int r = 0; r < M::NR; ++r) {
+            if (d->type[r] != M::kind(r) || (d->reversible[r] != 0) != (M::rev(r) != 0)) return false;
+            for (int k = 0; k < M::NS; ++k) {
+                if (d->nu_f[r * M::NS + k] != (double)M::nuf(r, k)) return false;
+                if (d->nu_r[r * M::NS + k] != (double)M::nur(r, k)) return false;
+            }
+            if (M::kind(r) != 0) {
+                int cnt = 0;
+                for (int k = 0; k < M::NS; ++k) {
+                    if (d->eff[r * M::NS + k] != 1.0) {
+                        if (cnt >= M::neff(r) || M::eff_sp(r, cnt) != k) return false;
+                        ++cnt;
+                    }
+                }
+                if (cnt != M::neff(r)) return false;
+            }
+            if (M::kind(r) == 3 && ((d->troe[4 * r + 3] > 0.0) != (M::troe_t2(r) != 0))) return false;
+        }
+        return true;
+    }
+
+    static void fill(const chem_mech_desc* d, void* out)
+    {
+        P& p = *static_cast<P*>(out);
+        std::memset(&p, 0, sizeof(P));
+        const int ns = M::NS, nr = M::NR;
+        double tmid0 = d->T_range[1];
+        bool common = true;
+        p.T_valid_lo = -1e300;
+        p.T_valid_hi = 1e300;
+        for (int k = 0; k < ns; ++k) {
+            p.W[k] = d->W[k];
+            p.invW[k] = 1.0 / d->W[k];
+            p.Tmid[k] = d->T_range[3 * k + 1];
+            common = common && (p.Tmid[k] == tmid0);
+            p.T_valid_lo = std::max(p.T_valid_lo, d->T_range[3 * k + 0]);
+            p.T_valid_hi = std::min(p.T_valid_hi, d->T_range[3 * k + 2]);
+            for (int rg = 0; rg < 2; ++rg) {
+                const double* a = (rg == 0 ? d->nasa_lo : d->nasa_hi) + 7 * k;
+                p.cpc[rg][k][0] = a[0]; p.cpc[rg][k][1] = a[1]; p.cpc[rg][k][2] = a[2];
+                p.cpc[rg][k][3] = a[3]; p.cpc[rg][k][4] = a[4];
+                p.hc[rg][k][0] = a[0]; p.hc[rg][k][1] = a[1] / 2; p.hc[rg][k][2] = a[2] / 3;
+                p.hc[rg][k][3] = a[3] / 4; p.hc[rg][k][4] = a[4] / 5; p.hc[rg][k][5] = a[5];
+                p.sc[rg][k][0] = a[0]; p.sc[rg][k][1] = a[1]; p.sc[rg][k][2] = a[2] / 2;
+                p.sc[rg][k][3] = a[3] / 3; p.sc[rg][k][4] = a[4] / 4; p.sc[rg][k][5] = a[6];
+                p.dcp[rg][k][0] = a[1]; p.dcp[rg][k][1] = 2 * a[2]; p.dcp[rg][k][2] = 3 * a[3];
+                p.dcp[rg][k][3] = 4 * a[4];
+            }
+        }
+        p.Tmid_common = common ? tmid0 : -1.0;
+        for (int r = 0; r < nr; ++r) {
+            p.lnA[r] = std::log(d->A[r]);
+            p.b[r] = d->b[r];
+            p.EaR[r] = d->Ea[r] / d->R;
+            if (M::kind(r) >= 2) {
+                p.lnA0[r] = std::log(d->A0[r]);
+                p.b0[r] = d->b0[r];
+                p.Ea0R[r] = d->Ea0[r] / d->R;
+            }
+            if (M::kind(r) == 3) {
+                const double* t = d->troe + 4 * r;
+                p.troe_a[r] = t[0];
+                p.troe_iT3[r] = t[1] != 0.0 ? std::min(1.0 / t[1], 1e300) : 1e300;
+                p.troe_iT1[r] = t[2] != 0.0 ? std::min(1.0 / t[2], 1e300) : 1e300;
+                p.troe_T2[r] = t[3];
+            }
+            for (int i = 0; i < M::neff(r); ++i) p.effm1[M::eff_off(r) + i] = d->eff[r * ns + M::eff_sp(r, i)] - 1.0;
+        }
+        p.R = d->R;
+        p.lnp0R = std::log(d->p_ref / d->R);
+    }
+
+    static cudaError_t rates(const void* pp, int64_t n, int64_t ld, const double* rho, const double* T,
+                             const double* Y, double* w, cudaStream_t s)
+    {
+        if (n == 0) return cudaSuccess;
+        k_rates<M><<<grid_for(n, kPointBS), kPointBS, 0, s>>>(*static_cast<const P*>(pp), n, ld, rho, T, Y, w);
+        return cudaGetLastError();
+    }
+    static cudaError_t rhs(const void* pp, int64_t n, int64_t ld, const double* rho, const double* T,
+                           const double* Y, double* f, cudaStream_t s)
+    {
+        if (n == 0) return cudaSuccess;
+        k_rhs<M><<<grid_for(n, kPointBS), kPointBS, 0, s>>>(*static_cast<const P*>(pp), n, ld, rho, T, Y, f);
+        return cudaGetLastError();
+    }
+    static cudaError_t jacobian(const void* pp, int64_t n, int64_t ld, const double* rho, const double* T,
+                                const double* Y, double* J, cudaStream_t s)
+    {
+        if (n == 0) return cudaSuccess;
+        constexpr int BS = 32;
+        const size_t sm = (size_t)(M::NS + 1) * (M::NS + 1) * 8 * BS;
+        cudaError_t e = cudaFuncSetAttribute(k_jacobian<M, BS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        if (e != cudaSuccess) return e;
+        k_jacobian<M, BS><<<(unsigned)((n + BS - 1) / BS), BS, sm, s>>>(*static_cast<const P*>(pp), n, ld, rho, T, Y, J);
+        return cudaGetLastError();
+    }
+    static cudaError_t temperature(const void* pp, int64_t n, int64_t ld, const double* e, const double* Y,
+                                   double* T, unsigned long long* nfail, cudaStream_t s)
+    {
+        if (n == 0) return cudaSuccess;
+        k_temperature<M><<<grid_for(n, kPointBS), kPointBS, 0, s>>>(*static_cast<const P*>(pp), n, ld, e, Y, T, nfail);
+        return cudaGetLastError();
+    }
+    static cudaError_t energy(const void* pp, int64_t n, int64_t ld, const double* T, const double* Y, double* e,
+                              cudaStream_t s)
+    {
+        if (n == 0) return cudaSuccess;
+        k_energy<M><<<grid_for(n, kPointBS), kPointBS, 0, s>>>(*static_cast<const P*>(pp), n, ld, T, Y, e);
+        return cudaGetLastError();
+    }
+
+    static constexpr size_t smem() { return (size_t)SmemLayout<M>::bytes_per_thread * kIntegrateBS; }
+
+    template <class Meth>
+    static cudaError_t launch(const P& p, const LaunchCtx& L, const uint32_t* ids, int64_t n, int kmax, int refill,
+                              int fin, int grid, cudaStream_t s)
+    {
+        auto kern = k_integrate<M, Meth, kIntegrateBS>;
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem());
+        if (e != cudaSuccess) return e;
+        kern<<<grid, kIntegrateBS, smem(), s>>>(p, L, ids, n, kmax, refill, fin);
+        return cudaGetLastError();
+    }
+    static cudaError_t integrate(const void* pp, int method, const LaunchCtx& L, const uint32_t* ids, int64_t n,
+                                 int kmax, int refill, int fin, int grid, cudaStream_t s)
+    {
+        const P& p = *static_cast<const P*>(pp);
+        if (method == CHEM_METHOD_RODAS3) return launch<Rodas3>(p, L, ids, n, kmax, refill, fin, grid, s);
+        return launch<Rodas4>(p, L, ids, n, kmax, refill, fin, grid, s);
+    }
+    template <class Meth>
+    static int bps()
+    {
+        int nb = 0;
+        auto kern = k_integrate<M, Meth, kIntegrateBS>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem());
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kIntegrateBS, smem());
+        return std::max(nb, 1);
+    }
+    static int blocks_per_sm(int method) { return method == CHEM_METHOD_RODAS3 ? bps<Rodas3>() : bps<Rodas4>(); }
+
+    static Ops ops()
+    {
+        Ops o;
+        o.name = M::kName;
+        o.ns = M::NS;
+        o.nr = M::NR;
+        o.nsa = M::NSA;
+        o.params_size = sizeof(P);
+        o.match = &match;
+        o.fill = &fill;
+        o.rates = &rates;
+        o.rhs = &rhs;
+        o.jacobian = &jacobian;
+        o.temperature = &temperature;
+        o.energy = &energy;
+        o.integrate = &integrate;
+        o.blocks_per_sm = &blocks_per_sm;
+        o.integrate_smem = smem();
+        return o;
+    }
+};
+
+const std::vector<Ops>& registry()
+{
+    static std::vector<Ops> r = [] {
+        std::vector<Ops> v;
+#define CHEM_REG(M) v.push_back(MechOps<M>::ops());
+        CHEM_FOR_EACH_MECH(CHEM_REG)
+#undef CHEM_REG
+        return v;
+    }();
+    return r;
+}
+
+// ------------------------------------------------------------------ validation
+int validate(const chem_mech_desc* d)
+{
+    if (!d || d->ns < 1 || d->ns > 32 || d->nr < 0 || d->ne < 1) return CHEM_EINVAL;
+    if (!d->W || !d->nasa_lo || !d->nasa_hi || !d->T_range || !d->elem || (d->nr > 0 && (!d->nu_f || !d->nu_r ||
+        !d->A || !d->b || !d->Ea || !d->type || !d->reversible || !d->eff || !d->A0 || !d->b0 || !d->Ea0 || !d->troe)))
+        return CHEM_EINVAL;
+    if (!(d->R > 0.0) || !(d->p_ref > 0.0)) return CHEM_EMECH;
+    const int ns = d->ns;
+    for (int k = 0; k < ns; ++k) {
+        if (!(d->W[k] > 0.0) || !std::isfinite(d->W[k])) return CHEM_EMECH;
+        const double* t = d->T_range + 3 * k;
+        if (!(t[0] < t[1] && t[1] < t[2])) return CHEM_EMECH;
+        for (int i = 0; i < 7; ++i)
+            if (!std::isfinite(d->nasa_lo[7 * k + i]) || !std::isfinite(d->nasa_hi[7 * k + i])) return CHEM_EMECH;
+    }
+    for (int r = 0; r < d->nr; ++r) {
+        if (d->type[r] < 0 || d->type[r] > 3) return CHEM_EMECH;
+        if (!(d->A[r] > 0.0) || !std::isfinite(d->b[r]) || !std::isfinite(d->Ea[r])) return CHEM_EMECH;
+        if (d->type[r] >= 2 && !(d->A0[r] > 0.0)) return CHEM_EMECH;
+        double dm = 0.0, gm = 0.0;
+        for (int k = 0; k < ns; ++k) {
+            const double f = d->nu_f[r * ns + k], b = d->nu_r[r * ns + k];
+            if (f < 0 || b < 0 || f != std::floor(f) || b != std::floor(b)) return CHEM_EMECH;
+            if (d->eff[r * ns + k] < 0.0) return CHEM_EMECH;
+            dm += (b - f) * d->W[k];
+            gm += (b + f) * d->W[k];
+        }
+        if (std::fabs(dm) > 1e-10 * gm) return CHEM_EMECH;
+        for (int e = 0; e < d->ne; ++e) {
+            double s = 0.0;
+            for (int k = 0; k < ns; ++k) s += (d->nu_r[r * ns + k] - d->nu_f[r * ns + k]) * d->elem[k * d->ne + e];
+            if (s != 0.0) return CHEM_EMECH;
+        }
+    }
+    return CHEM_OK;
+}
+
+// ------------------------------------------------------------------ workspace layout
+struct WsLayout {
+    size_t stats, boxes, start, cell_t, cell_h, steps, state, ids0, idsA, idsB, total;
+};
+
+inline size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+WsLayout ws_layout(int64_t N, int32_t B)
+{
+    WsLayout w;
+    size_t o = 0;
+    w.stats = o; o = al256(o + S_NSTATS * 8);
+    w.boxes = o; o = al256(o + (size_t)B * sizeof(DevBox));
+    w.start = o; o = al256(o + (size_t)(B + 1) * 8);
+    w.cell_t = o; o = al256(o + (size_t)N * 8);
+    w.cell_h = o; o = al256(o + (size_t)N * 8);
+    w.steps = o; o = al256(o + (size_t)N * 4);
+    w.state = o; o = al256(o + (size_t)N);
+    w.ids0 = o; o = al256(o + (size_t)N * 4);
+    w.idsA = o; o = al256(o + (size_t)N * 4);
+    w.idsB = o; o = al256(o + (size_t)N * 4);
+    w.total = o;
+    return w;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ the context
+struct chem_ctx {
+    int device = 0;
+    const Ops* ops = nullptr;
+    std::vector<unsigned char> params;
+    chem_opts opts;
+    int num_sms = 148;
+    int sticky = 0;
+    int32_t h_cap = 0;
+    DevBox* h_boxes = nullptr;        // pinned
+    int64_t* h_start = nullptr;       // pinned
+    unsigned long long* h_stats = nullptr;  // pinned [S_NSTATS]
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+};
+
+namespace {
+
+int cuda_fail(chem_ctx* c, cudaError_t e)
+{
+    if (e == cudaSuccess) return CHEM_OK;
+    if (c) c->sticky = CHEM_ECUDA;
+    std::fprintf(stderr, "libchem: CUDA error %s\n", cudaGetErrorString(e));
+    return CHEM_ECUDA;
+}
+
+int ensure_host_boxes(chem_ctx* c, int32_t nb)
+{
+    if (nb <= c->h_cap) return CHEM_OK;
+    if (c->h_boxes) cudaFreeHost(c->h_boxes);
+    if (c->h_start) cudaFreeHost(c->h_start);
+    c->h_boxes = nullptr;
+    c->h_start = nullptr;
+    int cap = std::max(nb, 64);
+    if (cudaMallocHost(&c->h_boxes, sizeof(DevBox) * cap) != cudaSuccess) return CHEM_ECUDA;
+    if (cudaMallocHost(&c->h_start, sizeof(int64_t) * (cap + 1)) != cudaSuccess) return CHEM_ECUDA;
+    c->h_cap = cap;
+    return CHEM_OK;
+}
+
+float elapsed(chem_ctx* c)
+{
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
+    return ms;
+}
+
+}  // namespace
+
+extern "C" {
+
+void chem_default_opts(chem_opts* o)
+{
+    if (!o) return;
+    o->T_min = 500.0;
+    o->kmax_bulk = 5;
+    o->n_active_star = 10000;
+    o->kmax_sparse = 100000;
+    o->atol_T = 1e-6;
+    o->method = CHEM_METHOD_RODAS4;
+    o->compact_bulk = 1;
+}
+
+const char* chem_strerror(int code)
+{
+    switch (code) {
+    case CHEM_OK: return "ok";
+    case CHEM_EINVAL: return "invalid argument";
+    case CHEM_EMECH: return "mechanism tables fail validation";
+    case CHEM_ENOSTRUCT: return "mechanism reaction structure is not compiled into libchem (run gen_structure, rebuild)";
+    case CHEM_ECUDA: return "CUDA error";
+    case CHEM_ENOWS: return "workspace too small";
+    default: return "unknown error";
+    }
+}
+
+static int check_opts(const chem_opts* o)
+{
+    if (o->kmax_bulk < 1 || o->kmax_sparse < 1 || o->n_active_star < 0 || !(o->atol_T > 0.0) ||
+        (o->method != CHEM_METHOD_RODAS4 && o->method != CHEM_METHOD_RODAS3) || !std::isfinite(o->T_min))
+        return CHEM_EINVAL;
+    return CHEM_OK;
+}
+
+int chem_init(const chem_mech_desc* mech, const chem_opts* opts, int device, chem_ctx** out)
+{
+    if (!out) return CHEM_EINVAL;
+    *out = nullptr;
+    int rc = validate(mech);
+    if (rc != CHEM_OK) return rc;
+    chem_opts o;
+    chem_default_opts(&o);
+    if (opts) o = *opts;
+    if (check_opts(&o) != CHEM_OK) return CHEM_EINVAL;
+    const Ops* ops = nullptr;
+    for (const Ops& x : registry())
+        if (x.match(mech)) { ops = &x; break; }
+    if (!ops) return CHEM_ENOSTRUCT;
+    if (cudaSetDevice(device) != cudaSuccess) return CHEM_ECUDA;
+    chem_ctx* c = new (std::nothrow) chem_ctx();
+    if (!c) return CHEM_ECUDA;
+    c->device = device;
+    c->ops = ops;
+    c->opts = o;
+    c->params.resize(ops->params_size);
+    ops->fill(mech, c->params.data());
+    cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+    if (cudaMallocHost(&c->h_stats, sizeof(unsigned long long) * S_NSTATS) != cudaSuccess ||
+        cudaEventCreate(&c->ev[0]) != cudaSuccess || cudaEventCreate(&c->ev[1]) != cudaSuccess ||
+        ensure_host_boxes(c, 64) != CHEM_OK) {
+        chem_finalize(c);
+        return CHEM_ECUDA;
+    }
+    *out = c;
+    return CHEM_OK;
+}
+
+void chem_finalize(chem_ctx* c)
+{
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->h_boxes) cudaFreeHost(c->h_boxes);
+    if (c->h_start) cudaFreeHost(c->h_start);
+    if (c->h_stats) cudaFreeHost(c->h_stats);
+    for (auto& e : c->ev)
+        if (e) cudaEventDestroy(e);
+    delete c;
+}
+
+const char* chem_structure_name(const chem_ctx* c) { return (c && c->ops) ? c->ops->name : ""; }
+
+int chem_set_opts(chem_ctx* c, const chem_opts* o)
+{
+    if (!c || !o || check_opts(o) != CHEM_OK) return CHEM_EINVAL;
+    c->opts = *o;
+    return CHEM_OK;
+}
+
+size_t chem_workspace_bytes(const chem_ctx* c, int64_t max_cells, int32_t max_boxes)
+{
+    if (!c || max_cells < 0 || max_boxes < 1) return 0;
+    return ws_layout(max_cells, max_boxes).total;
+}
+
+#define CHEM_PRE(c)                                        \
+    do {                                                   \
+        if (!(c)) return CHEM_EINVAL;                      \
+        if ((c)->sticky) return (c)->sticky;               \
+        if (cudaSetDevice((c)->device) != cudaSuccess) return CHEM_ECUDA; \
+    } while (0)
+
+int chem_rates(chem_ctx* c, int64_t n, int64_t ld, const double* rho, const double* T, const double* Y,
+               double* wdot, void* stream)
+{
+    CHEM_PRE(c);
+    if (n < 0 || ld < n || (n > 0 && (!rho || !T || !Y || !wdot))) return CHEM_EINVAL;
+    return cuda_fail(c, c->ops->rates(c->params.data(), n, ld, rho, T, Y, wdot, (cudaStream_t)stream));
+}
+
+int chem_rhs(chem_ctx* c, int64_t n, int64_t ld, const double* rho, const double* T, const double* Y, double* f,
+             void* stream)
+{
+    CHEM_PRE(c);
+    if (n < 0 || ld < n || (n > 0 && (!rho || !T || !Y || !f))) return CHEM_EINVAL;
+    return cuda_fail(c, c->ops->rhs(c->params.data(), n, ld, rho, T, Y, f, (cudaStream_t)stream));
+}
+
+int chem_jacobian(chem_ctx* c, int64_t n, int64_t ld, const double* rho, const double* T, const double* Y,
+                  double* J, void* stream)
+{
+    CHEM_PRE(c);
+    if (n < 0 || ld < n || (n > 0 && (!rho || !T || !Y || !J))) return CHEM_EINVAL;
+    return cuda_fail(c, c->ops->jacobian(c->params.data(), n, ld, rho, T, Y, J, (cudaStream_t)stream));
+}
+
+int chem_temperature(chem_ctx* c, int64_t n, int64_t ld, const double* e, const double* Y, double* T, void* stream)
+{
+    CHEM_PRE(c);
+    if (n < 0 || ld < n || (n > 0 && (!e || !Y || !T))) return CHEM_EINVAL;
+    return cuda_fail(c, c->ops->temperature(c->params.data(), n, ld, e, Y, T, nullptr, (cudaStream_t)stream));
+}
+
+int chem_energy(chem_ctx* c, int64_t n, int64_t ld, const double* T, const double* Y, double* e, void* stream)
+{
+    CHEM_PRE(c);
+    if (n < 0 || ld < n || (n > 0 && (!e || !Y || !T))) return CHEM_EINVAL;
+    return cuda_fail(c, c->ops->energy(c->params.data(), n, ld, T, Y, e, (cudaStream_t)stream));
+}
+
+int chem_integrate(chem_ctx* c, int64_t n, int64_t ld, const double* rho, const double* e, double* T, double* Y,
+                   const uint8_t* solid, double dt, double rtol, double atol, void* ws, size_t ws_bytes,
+                   chem_stats* stats, void* stream)
+{
+    chem_box b;
+    b.rho = rho;
+    b.e = e;
+    b.T = T;
+    b.Y = Y;
+    b.solid = solid;
+    b.ncells = n;
+    b.ld = ld;
+    b.dt = dt;
+    return chem_integrate_boxes(c, 1, &b, rtol, atol, ws, ws_bytes, nullptr, stats, stream);
+}
+
+int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, double rtol, double atol, void* ws,
+                         size_t ws_bytes, double* box_cost, chem_stats* stats, void* stream)
+{
+    CHEM_PRE(c);
+    if (nboxes < 1 || !boxes || !(rtol > 0.0) || !(atol > 0.0) || !ws) return CHEM_EINVAL;
+    int64_t total = 0;
+    for (int b = 0; b < nboxes; ++b) {
+        const chem_box& x = boxes[b];
+        if (x.ncells < 0 || x.ld < x.ncells || !(x.dt > 0.0) || !std::isfinite(x.dt)) return CHEM_EINVAL;
+        if (x.ncells > 0 && (!x.rho || !x.e || !x.T || !x.Y)) return CHEM_EINVAL;
+        total += x.ncells;
+    }
+    if (total >= (int64_t)0xffffffffLL) return CHEM_EINVAL;  // 32-bit cell index map
+    const WsLayout W = ws_layout(total, nboxes);
+    if (ws_bytes < W.total) return CHEM_ENOWS;
+    if (ensure_host_boxes(c, nboxes) != CHEM_OK) return CHEM_ECUDA;
+    cudaStream_t s = (cudaStream_t)stream;
+    const chem_opts& o = c->opts;
+    const Ops& ops = *c->ops;
+    char* base = static_cast<char*>(ws);
+
+    int64_t acc = 0;
+    for (int b = 0; b < nboxes; ++b) {
+        const chem_box& x = boxes[b];
+        c->h_boxes[b] = DevBox{x.rho, x.e, x.T, x.Y, x.solid, x.ncells, x.ld, x.dt};
+        c->h_start[b] = acc;
+        acc += x.ncells;
+    }
+    c->h_start[nboxes] = acc;
+
+    LaunchCtx L;
+    L.boxes = reinterpret_cast<const DevBox*>(base + W.boxes);
+    L.box_start = reinterpret_cast<const int64_t*>(base + W.start);
+    L.nboxes = nboxes;
+    L.total = total;
+    L.cell_t = reinterpret_cast<double*>(base + W.cell_t);
+    L.cell_h = reinterpret_cast<double*>(base + W.cell_h);
+    L.state = reinterpret_cast<uint8_t*>(base + W.state);
+    L.cell_steps = reinterpret_cast<int32_t*>(base + W.steps);
+    L.stats = reinterpret_cast<unsigned long long*>(base + W.stats);
+    L.rtol = rtol;
+    L.atol = atol;
+    L.atolT = o.atol_T;
+    L.T_min = o.T_min;
+    uint32_t* ids0 = reinterpret_cast<uint32_t*>(base + W.ids0);
+    uint32_t* idsA = reinterpret_cast<uint32_t*>(base + W.idsA);
+    uint32_t* idsB = reinterpret_cast<uint32_t*>(base + W.idsB);
+
+    chem_stats st;
+    std::memset(&st, 0, sizeof(st));
+    st.cells = total;
+    cudaError_t e;
+#define CK(x)                                        \
+    do {                                             \
+        if ((e = (x)) != cudaSuccess) return cuda_fail(c, e); \
+    } while (0)
+
+    CK(cudaMemcpyAsync(base + W.boxes, c->h_boxes, sizeof(DevBox) * nboxes, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(base + W.start, c->h_start, sizeof(int64_t) * (nboxes + 1), cudaMemcpyHostToDevice, s));
+    CK(cudaMemsetAsync(L.stats, 0, S_NSTATS * 8, s));
+    if (box_cost) CK(cudaMemsetAsync(box_cost, 0, sizeof(double) * nboxes, s));
+    if (total == 0) {
+        CK(cudaStreamSynchronize(s));
+        if (stats) *stats = st;
+        return CHEM_OK;
+    }
+
+    auto read_count = [&](int64_t& v) -> cudaError_t {
+        cudaError_t r = cudaMemcpyAsync(c->h_stats + S_COUNT_ACTIVE, L.stats + S_COUNT_ACTIVE, 8,
+                                        cudaMemcpyDeviceToHost, s);
+        if (r != cudaSuccess) return r;
+        r = cudaStreamSynchronize(s);
+        v = (int64_t)c->h_stats[S_COUNT_ACTIVE];
+        return r;
+    };
+
+    // ---- Alg. 3 §1: gate + count + index map
+    CK(cudaEventRecord(c->ev[0], s));
+    k_gate<kStreamBS><<<grid_for(total, kStreamBS), kStreamBS, 0, s>>>(L, ids0);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(c->ev[1], s));
+    int64_t n_active = 0;
+    CK(read_count(n_active));
+    st.t_gate_ms = elapsed(c);
+    st.active0 = n_active;
+
+    // ---- Alg. 3 §2: bulk bursts while N_active > N*
+    const uint32_t* cur = ids0;
+    int64_t n_cur = n_active;
+    uint32_t* nxt = idsA;
+    while (n_cur > o.n_active_star && n_cur > 0) {
+        const bool all_cells = !o.compact_bulk;
+        const uint32_t* lst = all_cells ? nullptr : cur;
+        const int64_t nl = all_cells ? total : n_cur;
+        CK(cudaEventRecord(c->ev[0], s));
+        CK(ops.integrate(c->params.data(), o.method, L, lst, nl, o.kmax_bulk, 0, 0,
+                         (int)((nl + kIntegrateBS - 1) / kIntegrateBS), s));
+        CK(cudaEventRecord(c->ev[1], s));
+        CK(cudaEventSynchronize(c->ev[1]));
+        st.t_bulk_ms += elapsed(c);
+        CK(cudaEventRecord(c->ev[0], s));
+        CK(cudaMemsetAsync(L.stats + S_COUNT_ACTIVE, 0, 8, s));
+        k_compact<kStreamBS><<<grid_for(nl, kStreamBS), kStreamBS, 0, s>>>(L, lst, nl, nxt);
+        CK(cudaGetLastError());
+        CK(cudaEventRecord(c->ev[1], s));
+        CK(read_count(n_cur));
+        st.t_compact_ms += elapsed(c);
+        if (st.bulk_iters < 16) st.active_per_iter[st.bulk_iters] = n_cur;
+        st.bulk_iters++;
+        cur = nxt;
+        nxt = (nxt == idsA) ? idsB : idsA;
+    }
+
+    // ---- Alg. 3 §3: sparse integration over the index map (persistent, lane refill)
+    st.sparse_cells = n_cur;
+    if (n_cur > 0) {
+        const int grid = std::max(1, std::min<int>(c->num_sms * ops.blocks_per_sm(o.method),
+                                                   (int)((n_cur + kIntegrateBS - 1) / kIntegrateBS)));
+        CK(cudaMemsetAsync(L.stats + S_CURSOR, 0, 8, s));
+        CK(cudaEventRecord(c->ev[0], s));
+        CK(ops.integrate(c->params.data(), o.method, L, cur, n_cur, o.kmax_sparse, 1, 1, grid, s));
+        CK(cudaEventRecord(c->ev[1], s));
+    }
+    if (box_cost && n_active > 0) {
+        k_box_cost<kStreamBS><<<grid_for(n_active, kStreamBS), kStreamBS, 0, s>>>(L, ids0, n_active, box_cost);
+        CK(cudaGetLastError());
+    }
+    CK(cudaMemcpyAsync(c->h_stats, L.stats, S_NSTATS * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (n_cur > 0) st.t_sparse_ms = elapsed(c);
+    const unsigned long long* hs = c->h_stats;
+    st.steps_attempted = (int64_t)hs[S_ATTEMPTED];
+    st.steps_accepted = (int64_t)hs[S_ACCEPTED];
+    st.rhs_evals = (int64_t)hs[S_RHS];
+    st.jac_evals = (int64_t)hs[S_JAC];
+    st.lu_count = (int64_t)hs[S_LU];
+    st.n_newton_fail = (int64_t)hs[S_NEWTON_FAIL];
+    st.n_nonfinite = (int64_t)hs[S_NONFINITE];
+    st.n_T_range = (int64_t)hs[S_TRANGE];
+    st.n_unfinished = (int64_t)hs[S_UNFINISHED];
+    unsigned long long db = hs[S_DRIFT_BITS];
+    std::memcpy(&st.max_energy_drift, &db, 8);
+    if (stats) *stats = st;
+#undef CK
+    return CHEM_OK;
+}
+
+}  // extern "C"

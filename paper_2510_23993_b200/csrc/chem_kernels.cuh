@@ -1,0 +1,531 @@
+// chem_kernels.cuh — the sm_100a kernels of the bulk-sparse schedule (Alg. 3).
+//
+//   k_gate       A1/A2  gate + count + cell index map (ballot / block scan, one atomic per block)
+//   k_integrate  A1/A6/A7/A9  bulk burst (<= K_max substeps per cell, one thread per id) and the
+//                sparse launch (persistent grid; a lane whose cell finishes takes the next id from
+//                an atomic cursor, so warps stay full through the long tail)
+//   k_compact    A8     still-active ids -> next index map (ballot / block scan)
+//   k_box_cost   A10    per-box attempted substeps (box cost for load balancing)
+//   k_rates / k_rhs / k_jacobian / k_temperature / k_energy: point evaluations (C-ABI test hooks)
+//
+// Multi-box fusion (A10): a global cell id g indexes the concatenation of all boxes;
+// box b = upper_bound(box_start, g) - 1, offset = g - box_start[b].  One launch per phase spans
+// every box; no data is copied (the kernels read and write the caller's arrays in place).
+#pragma once
+#include "chem_device.cuh"
+
+namespace chem {
+
+enum CellState : uint8_t {
+    ST_INACTIVE = 0,   // gated out (T < T_min or solid): never touched
+    ST_FRESH = 1,      // active, not started (needs the initial Newton T)
+    ST_RUNNING = 2,    // active, t < dt, state persisted in the caller's arrays + workspace
+    ST_DONE = 3,       // reached t = dt
+    ST_UNFINISHED = 4, // sparse K_max exhausted (P:179 safeguard)
+    ST_FAILED = 5,     // Newton failure / non-finite / step-size underflow
+};
+
+enum StatIdx {
+    S_ATTEMPTED = 0, S_ACCEPTED, S_RHS, S_JAC, S_LU, S_NEWTON_FAIL, S_NONFINITE, S_TRANGE, S_UNFINISHED,
+    S_DONE, S_DRIFT_BITS, S_COUNT_ACTIVE, S_CURSOR, S_NSTATS
+};
+
+struct DevBox {
+    const double* rho;
+    const double* e;
+    double* T;
+    double* Y;
+    const uint8_t* solid;
+    int64_t ncells, ld;
+    double dt;
+};
+
+struct LaunchCtx {
+    const DevBox* boxes;
+    const int64_t* box_start;  // [nboxes + 1] prefix of ncells
+    int32_t nboxes;
+    int64_t total;
+    double* cell_t;            // [total] local time t_i
+    double* cell_h;            // [total] next substep size
+    uint8_t* state;            // [total] CellState (+ bit 7: last step rejected)
+    int32_t* cell_steps;       // [total] attempted substeps summed over launches
+    unsigned long long* stats; // [S_NSTATS]
+    double rtol, atol, atolT, T_min;
+};
+
+__device__ __forceinline__ int find_box(const LaunchCtx& L, int64_t g)
+{
+    int lo = 0, hi = L.nboxes - 1;
+    while (lo < hi) {  // last b with box_start[b] <= g
+        const int mid = (lo + hi + 1) >> 1;
+        if (__ldg(&L.box_start[mid]) <= g) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+// Full-warp add of a per-lane value to a device counter.  Every lane of the warp must call it
+// (callers __syncwarp() first); xor-shuffles with a partial mask would read inactive lanes.
+__device__ __forceinline__ void warp_add(unsigned long long* p, unsigned long long v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(p, v);
+}
+
+// Block-wide stream compaction helper: each thread has flag `keep` and id `g`; kept ids are
+// written to out[] at positions reserved with one atomicAdd per block.  Order within a block
+// follows thread order.  Requires all threads of the block to call it.
+template <int BS>
+__device__ __forceinline__ void block_compact(bool keep, uint32_t g, uint32_t* out, unsigned long long* counter)
+{
+    __shared__ int warp_cnt[BS / 32];
+    __shared__ unsigned long long base;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) warp_cnt[wid] = __popc(bal);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int s = 0;
+#pragma unroll
+        for (int w = 0; w < BS / 32; ++w) { const int c = warp_cnt[w]; warp_cnt[w] = s; s += c; }
+        base = s ? atomicAdd(counter, (unsigned long long)s) : 0ull;
+    }
+    __syncthreads();
+    if (keep) out[base + warp_cnt[wid] + __popc(bal & ((1u << lane) - 1u))] = g;
+    __syncthreads();
+}
+
+// ----------------------------------------------------------------------------- A2 gate + count
+template <int BS>
+__global__ void __launch_bounds__(BS) k_gate(LaunchCtx L, uint32_t* ids_out)
+{
+    for (int64_t base = (int64_t)blockIdx.x * BS; base < L.total; base += (int64_t)gridDim.x * BS) {
+        const int64_t g = base + threadIdx.x;
+        bool act = false;
+        if (g < L.total) {
+            const int b = find_box(L, g);
+            const DevBox bx = L.boxes[b];
+            const int64_t off = g - L.box_start[b];
+            const double T = bx.T[off];
+            act = (T >= L.T_min) && !(bx.solid && bx.solid[off]);   // Alg. 3 §1
+            L.state[g] = act ? ST_FRESH : ST_INACTIVE;
+            if (act) L.cell_steps[g] = 0;
+        }
+        block_compact<BS>(act, (uint32_t)g, ids_out, &L.stats[S_COUNT_ACTIVE]);
+    }
+}
+
+// ----------------------------------------------------------------------------- A8 compaction
+template <int BS>
+__global__ void __launch_bounds__(BS) k_compact(LaunchCtx L, const uint32_t* ids_in, int64_t n_in, uint32_t* ids_out)
+{
+    for (int64_t base = (int64_t)blockIdx.x * BS; base < n_in; base += (int64_t)gridDim.x * BS) {
+        const int64_t i = base + threadIdx.x;
+        uint32_t g = 0;
+        bool keep = false;
+        if (i < n_in) {
+            g = ids_in ? ids_in[i] : (uint32_t)i;
+            const uint8_t s = L.state[g] & 0x7f;
+            keep = (s == ST_RUNNING) || (s == ST_FRESH);
+        }
+        block_compact<BS>(keep, g, ids_out, &L.stats[S_COUNT_ACTIVE]);
+    }
+}
+
+// ----------------------------------------------------------------------------- A10 box cost
+template <int BS>
+__global__ void __launch_bounds__(BS) k_box_cost(LaunchCtx L, const uint32_t* ids, int64_t n, double* box_cost)
+{
+    // every lane iterates the same number of times so warp collectives see a full mask
+    for (int64_t base = (int64_t)blockIdx.x * BS; base < n; base += (int64_t)gridDim.x * BS) {
+        const int64_t i = base + threadIdx.x;
+        const bool valid = i < n;
+        const uint32_t g = valid ? ids[i] : 0u;
+        const int b = valid ? find_box(L, g) : -1;
+        const double v = valid ? (double)L.cell_steps[g] : 0.0;
+        const int b0 = __shfl_sync(0xffffffffu, b, 0);
+        if (__all_sync(0xffffffffu, !valid || b == b0)) {
+            double s = v;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            if ((threadIdx.x & 31) == 0 && b0 >= 0) atomicAdd(&box_cost[b0], s);
+        } else if (valid) {
+            atomicAdd(&box_cost[b], v);
+        }
+    }
+}
+
+// ----------------------------------------------------------------------------- A6/A7/A9 integrate
+// Per-thread shared memory: the n x n iteration matrix (I/(h gamma) - J, then its LU), an
+// n-vector scratch for the permuted right-hand side, and n pivot bytes.
+template <class M>
+struct SmemLayout {
+    static constexpr int n = M::NSA + 1;
+    static constexpr int doubles = n * n + n + (n + 7) / 8;
+    static constexpr int bytes_per_thread = doubles * 8;
+};
+
+struct Counters {
+    unsigned long long attempted = 0, accepted = 0, rhs = 0, jac = 0, lu = 0, newton_fail = 0, nonfinite = 0,
+                       trange = 0, unfinished = 0, done = 0;
+    double drift = 0.0;
+};
+
+template <class M>
+struct Cell {
+    double y[M::NSA + 1];  // integrated unknowns: reacting Y_k, T
+    double Yin[M::NS];     // all species (inert ones stay constant)
+    double rho, e, t, h, dt;
+    int b;
+    int64_t off, ld;
+    uint32_t g;
+    int k;                 // attempted substeps in this launch
+    bool rej;              // last step rejected (controller memory, persisted in state bit 7)
+};
+
+// One attempted Rosenbrock substep on cell C (A6).  Returns 1 accepted, 0 rejected, -1 failure.
+template <class M, class Meth>
+__device__ __forceinline__ int ros_step(const Params<M>& P, const LaunchCtx& L, Cell<M>& C, const SMat& A,
+                                        uint8_t* piv, int pstride, double* scratch, int sstride, Counters& cnt)
+{
+    constexpr int n = M::NSA + 1;
+    constexpr int S = Meth::S;
+    const double invrho = 1.0 / C.rho;
+    double f0[n];
+    rhs_jac<M, false>(P, C.rho, C.y, C.Yin, f0, A);
+    cnt.rhs++;
+    cnt.jac++;
+    double sc[n];
+#pragma unroll
+    for (int i = 0; i < n; ++i) sc[i] = ((i < M::NSA) ? L.atol : L.atolT) + L.rtol * fabs(C.y[i]);
+    const double remaining = C.dt - C.t;
+    if (!(C.h > 0.0)) {
+        // initial step: 1% of the time for y to change by its own size (Hairer-Norsett-Wanner
+        // I.II.4 d0/d1 heuristic), capped at dt; a frozen or equilibrated cell takes one step.
+        double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+        for (int i = 0; i < n; ++i) {
+            d0 = fma(C.y[i] / sc[i], C.y[i] / sc[i], d0);
+            d1 = fma(f0[i] / sc[i], f0[i] / sc[i], d1);
+        }
+        d0 = sqrt(d0 / n);
+        d1 = sqrt(d1 / n);
+        C.h = (d0 < 1e-5 || d1 < 1e-5) ? remaining : fmin(remaining, 0.01 * d0 / d1);
+    }
+    bool last = false;
+    double h = C.h;
+    if (h >= remaining) { h = remaining; last = true; }
+    if (!(h > 4.0 * 2.220446049250313e-16 * C.dt) || !isfinite(h)) return -1;  // step-size underflow
+
+    // iteration matrix A = I/(h gamma) - J, LU in place
+    const double ghinv = 1.0 / (h * Meth::gamma);
+#pragma unroll
+    for (int i = 0; i < n; ++i)
+#pragma unroll
+        for (int j = 0; j < n; ++j) A(i, j) = (i == j) ? ghinv - A(i, j) : -A(i, j);
+    const bool ok = lu_factor<n>(A, piv, pstride);
+    cnt.lu++;
+
+    double K[S][n];
+    const double hinv = 1.0 / h;
+    static_for<0, S>([&](auto s_) {
+        constexpr int s = decltype(s_)::value;
+        double F[n];
+        if constexpr (s == 0 || !Meth::newf(s)) {
+#pragma unroll
+            for (int i = 0; i < n; ++i) F[i] = f0[i];
+        } else {
+            double ys[n];
+#pragma unroll
+            for (int i = 0; i < n; ++i) {
+                double v = C.y[i];
+                static_for<0, s>([&](auto j_) {
+                    constexpr int j = decltype(j_)::value;
+                    if constexpr (Meth::a(s, j) != 0.0) v = fma(Meth::a(s, j), K[j][i], v);
+                });
+                ys[i] = v;
+            }
+            rhs<M>(P, C.rho, invrho, ys, C.Yin, F);
+            cnt.rhs++;
+        }
+#pragma unroll
+        for (int i = 0; i < n; ++i) {
+            double v = F[i];
+            static_for<0, s>([&](auto j_) {
+                constexpr int j = decltype(j_)::value;
+                if constexpr (Meth::c(s, j) != 0.0) v = fma(Meth::c(s, j) * hinv, K[j][i], v);
+            });
+            K[s][i] = v;
+        }
+        lu_solve<n>(A, piv, pstride, scratch, sstride, K[s]);
+    });
+
+    double ynew[n];
+    double err = 0.0;
+#pragma unroll
+    for (int i = 0; i < n; ++i) {
+        double v = C.y[i], ev = 0.0;
+        static_for<0, S>([&](auto j_) {
+            constexpr int j = decltype(j_)::value;
+            if constexpr (Meth::m(j) != 0.0) v = fma(Meth::m(j), K[j][i], v);
+            if constexpr (Meth::e(j) != 0.0) ev = fma(Meth::e(j), K[j][i], ev);
+        });
+        ynew[i] = v;
+        const double s = ((i < M::NSA) ? L.atol : L.atolT) + L.rtol * fmax(fabs(C.y[i]), fabs(v));
+        err = fma(ev / s, ev / s, err);
+    }
+    err = sqrt(err / n);
+    cnt.attempted++;
+    C.k++;
+    if (!ok || !isfinite(err)) {  // singular matrix or non-finite stage: shrink hard, retry
+        C.h = h * 0.1;
+        C.rej = true;
+        return 0;
+    }
+    // step-size controller (Hairer-Wanner IV.8; KPP Rosenbrock): safety 0.9, factor in [0.2, 6]
+    double fac = 0.9 * pow(err, -Meth::err_exp);
+    fac = fmin(6.0, fmax(0.2, fac));
+    double hnew = h * fac;
+    if (err <= 1.0) {
+        cnt.accepted++;
+#pragma unroll
+        for (int i = 0; i < n; ++i) C.y[i] = ynew[i];
+        C.t = last ? C.dt : C.t + h;
+        if (C.rej) hnew = fmin(hnew, h);
+        C.rej = false;
+        C.h = hnew;
+        return 1;
+    }
+    C.h = C.rej ? h * 0.1 : hnew;  // repeated rejection: factor 0.1
+    C.rej = true;
+    return 0;
+}
+
+template <class M>
+__device__ __forceinline__ void load_cell(const Params<M>& P, const LaunchCtx& L, uint32_t g, Cell<M>& C,
+                                          uint8_t st, Counters& cnt, bool& ok)
+{
+    C.g = g;
+    C.b = find_box(L, g);
+    const DevBox bx = L.boxes[C.b];
+    C.off = g - L.box_start[C.b];
+    C.ld = bx.ld;
+    C.dt = bx.dt;
+    C.rho = bx.rho[C.off];
+    C.e = bx.e[C.off];
+#pragma unroll
+    for (int k = 0; k < M::NS; ++k) C.Yin[k] = bx.Y[k * C.ld + C.off];   // coalesced: consecutive ids
+#pragma unroll
+    for (int i = 0; i < M::NSA; ++i) C.y[i] = C.Yin[M::act(i)];
+    double T = bx.T[C.off];
+    C.k = 0;
+    ok = true;
+    if ((st & 0x7f) == ST_FRESH) {
+        // initial temperature from (e, Y) at constant (e, rho), seeded with the input T
+        if (!newton_T<M>(P, C.e, C.Yin, T)) { cnt.newton_fail++; ok = false; }
+        C.t = 0.0;
+        C.h = 0.0;
+        C.rej = false;
+    } else {
+        C.t = L.cell_t[g];
+        C.h = L.cell_h[g];
+        C.rej = (st & 0x80) != 0;
+    }
+    C.y[M::NSA] = T;
+}
+
+// Write back: running cells persist (Y, T_int) in place and (t, h, flags) in the workspace;
+// finished cells store Y_out and T_out = Newton(e, Y_out) (SURVEY reading 3).
+template <class M>
+__device__ __forceinline__ void store_cell(const Params<M>& P, const LaunchCtx& L, Cell<M>& C, uint8_t st,
+                                           Counters& cnt)
+{
+    const DevBox bx = L.boxes[C.b];
+#pragma unroll
+    for (int i = 0; i < M::NSA; ++i) bx.Y[M::act(i) * C.ld + C.off] = C.y[i];
+    double T = C.y[M::NSA];
+    if (st == ST_DONE || st == ST_UNFINISHED) {
+        double Yf[M::NS];
+        full_Y<M>(C.y, C.Yin, Yf);
+        const double Tint = T;
+        if (!newton_T<M>(P, C.e, Yf, T)) { cnt.newton_fail++; st = ST_FAILED; }
+        if (st == ST_DONE) {
+            cnt.done++;
+            cnt.drift = fmax(cnt.drift, fabs(Tint - T) / T);
+            if (T < P.T_valid_lo || T > P.T_valid_hi) cnt.trange++;
+        } else {
+            cnt.unfinished++;
+        }
+    }
+    bx.T[C.off] = T;
+    L.cell_t[C.g] = C.t;
+    L.cell_h[C.g] = C.h;
+    L.state[C.g] = st | (C.rej ? 0x80 : 0);
+    L.cell_steps[C.g] += C.k;
+}
+
+__device__ __forceinline__ void flush_counters(const LaunchCtx& L, Counters& c)
+{
+    warp_add(&L.stats[S_ATTEMPTED], c.attempted);
+    warp_add(&L.stats[S_ACCEPTED], c.accepted);
+    warp_add(&L.stats[S_RHS], c.rhs);
+    warp_add(&L.stats[S_JAC], c.jac);
+    warp_add(&L.stats[S_LU], c.lu);
+    warp_add(&L.stats[S_NEWTON_FAIL], c.newton_fail);
+    warp_add(&L.stats[S_NONFINITE], c.nonfinite);
+    warp_add(&L.stats[S_TRANGE], c.trange);
+    warp_add(&L.stats[S_UNFINISHED], c.unfinished);
+    warp_add(&L.stats[S_DONE], c.done);
+    // max drift: non-negative doubles order like their bit patterns
+    unsigned long long bits = __double_as_longlong(c.drift);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long v = __shfl_xor_sync(0xffffffffu, bits, o);
+        bits = v > bits ? v : bits;
+    }
+    if ((threadIdx.x & 31) == 0 && bits) atomicMax(&L.stats[S_DRIFT_BITS], bits);
+}
+
+// Bulk (refill = false): thread i takes ids[i] (identity when ids == nullptr, the paper's
+// all-cells launch) and runs <= kmax attempted substeps.  Sparse (refill = true): persistent
+// grid; each lane pulls ids from the atomic cursor S_CURSOR until the list is exhausted.
+// Both modes run the same substep code, so results are bitwise independent of K_max and N*.
+template <class M, class Meth, int BS>
+__global__ void __launch_bounds__(BS) k_integrate(const __grid_constant__ Params<M> P, LaunchCtx L,
+                                                  const uint32_t* __restrict__ ids, int64_t n_ids, int kmax,
+                                                  int refill, int final_phase)
+{
+    extern __shared__ double smem[];
+    constexpr int n = M::NSA + 1;
+    double* mine = smem + threadIdx.x;
+    SMat A{mine, BS, n};
+    double* scratch = mine + n * n * BS;
+    uint8_t* piv = reinterpret_cast<uint8_t*>(smem + (n * n + n) * BS) + threadIdx.x;
+
+    Counters cnt;
+    Cell<M> C;
+    bool have = false;
+    bool first = true;
+    for (;;) {
+        if (!have) {
+            int64_t idx;
+            if (refill) {
+                idx = (int64_t)atomicAdd(&L.stats[S_CURSOR], 1ull);
+            } else {
+                idx = first ? (int64_t)blockIdx.x * BS + threadIdx.x : n_ids;
+                first = false;
+            }
+            if (idx >= n_ids) break;
+            const uint32_t g = ids ? ids[idx] : (uint32_t)idx;
+            const uint8_t st = L.state[g];
+            if ((st & 0x7f) != ST_FRESH && (st & 0x7f) != ST_RUNNING) continue;
+            bool ok;
+            load_cell<M>(P, L, g, C, st, cnt, ok);
+            if (!ok) { L.state[g] = ST_FAILED; continue; }
+            have = true;
+        }
+        const int r = ros_step<M, Meth>(P, L, C, A, piv, BS, scratch, BS, cnt);
+        if (r < 0) {
+            cnt.nonfinite++;
+            store_cell<M>(P, L, C, ST_FAILED, cnt);
+            have = false;
+        } else if (C.t >= C.dt) {
+            store_cell<M>(P, L, C, ST_DONE, cnt);
+            have = false;
+        } else if (C.k >= kmax) {
+            store_cell<M>(P, L, C, final_phase ? ST_UNFINISHED : ST_RUNNING, cnt);
+            have = false;
+        }
+    }
+    __syncwarp();   // all lanes of the warp reach here (no early returns): reconverge for the reduction
+    flush_counters(L, cnt);
+}
+
+// ----------------------------------------------------------------------------- point kernels
+template <class M>
+__global__ void k_rates(const __grid_constant__ Params<M> P, int64_t n, int64_t ld, const double* __restrict__ rho,
+                        const double* __restrict__ T, const double* __restrict__ Y, double* __restrict__ wdot)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        double Yc[M::NS];
+#pragma unroll
+        for (int k = 0; k < M::NS; ++k) Yc[k] = Y[k * ld + i];
+        RateCtx<M> rc;
+        rate_ctx<M>(P, rho[i], T[i], Yc, rc);
+        double w[M::NS];
+        rates_from_ctx<M>(P, rc, w);
+#pragma unroll
+        for (int k = 0; k < M::NS; ++k) wdot[k * ld + i] = w[k];
+    }
+}
+
+template <class M>
+__global__ void k_rhs(const __grid_constant__ Params<M> P, int64_t n, int64_t ld, const double* __restrict__ rho,
+                      const double* __restrict__ T, const double* __restrict__ Y, double* __restrict__ f)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        double Yc[M::NS], y[M::NSA + 1], fo[M::NSA + 1];
+#pragma unroll
+        for (int k = 0; k < M::NS; ++k) Yc[k] = Y[k * ld + i];
+#pragma unroll
+        for (int a = 0; a < M::NSA; ++a) y[a] = Yc[M::act(a)];
+        y[M::NSA] = T[i];
+        rhs<M>(P, rho[i], 1.0 / rho[i], y, Yc, fo);
+#pragma unroll
+        for (int k = 0; k < M::NS; ++k) f[k * ld + i] = (M::act_of(k) >= 0) ? fo[M::act_of(k) >= 0 ? M::act_of(k) : 0] : 0.0;
+        f[M::NS * ld + i] = fo[M::NSA];
+    }
+}
+
+// Full (ns+1)^2 Jacobian, J[(r*(ns+1) + c)*ld + i]; staged through per-thread shared memory.
+template <class M, int BS>
+__global__ void __launch_bounds__(BS) k_jacobian(const __grid_constant__ Params<M> P, int64_t n, int64_t ld,
+                                                 const double* __restrict__ rho, const double* __restrict__ T,
+                                                 const double* __restrict__ Y, double* __restrict__ J)
+{
+    extern __shared__ double smem[];
+    constexpr int nn = M::NS + 1;
+    SMat A{smem + threadIdx.x, BS, nn};
+    const int64_t i = (int64_t)blockIdx.x * BS + threadIdx.x;
+    if (i >= n) return;
+    double y[nn], f[nn], Yd[M::NS];
+#pragma unroll
+    for (int k = 0; k < M::NS; ++k) { y[k] = Y[k * ld + i]; Yd[k] = y[k]; }
+    y[M::NS] = T[i];
+    rhs_jac<M, true>(P, rho[i], y, Yd, f, A);
+#pragma unroll
+    for (int r = 0; r < nn; ++r)
+#pragma unroll
+        for (int c = 0; c < nn; ++c) J[(int64_t)(r * nn + c) * ld + i] = A(r, c);
+}
+
+template <class M>
+__global__ void k_temperature(const __grid_constant__ Params<M> P, int64_t n, int64_t ld, const double* __restrict__ e,
+                              const double* __restrict__ Y, double* __restrict__ T,
+                              unsigned long long* __restrict__ nfail)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        double Yc[M::NS];
+#pragma unroll
+        for (int k = 0; k < M::NS; ++k) Yc[k] = Y[k * ld + i];
+        double t = T[i];
+        if (!newton_T<M>(P, e[i], Yc, t) && nfail) atomicAdd(nfail, 1ull);
+        T[i] = t;
+    }
+}
+
+template <class M>
+__global__ void k_energy(const __grid_constant__ Params<M> P, int64_t n, int64_t ld, const double* __restrict__ T,
+                         const double* __restrict__ Y, double* __restrict__ e)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        double Yc[M::NS];
+#pragma unroll
+        for (int k = 0; k < M::NS; ++k) Yc[k] = Y[k * ld + i];
+        double u, cv;
+        energy_cv<M>(P, T[i], Yc, u, cv);
+        e[i] = u;
+    }
+}
+
+}  // namespace chem

@@ -1,0 +1,90 @@
+"""CPU-side checks of the C ABI: libchem.so loads (CUDA runtime present, no device needed) and
+exports every symbol include/chem.h declares; the header and the binding agree; the product
+package does not import the oracle.  No compute calls (there is no GPU here)."""
+import ctypes
+import pathlib
+import re
+import subprocess
+import sys
+
+import pytest
+
+ROOT = pathlib.Path(__file__).resolve().parent.parent
+
+
+def _declared():
+    text = (ROOT / "include" / "chem.h").read_text()
+    decl = re.findall(r"^\s*(?:int|void|size_t|const char\s*\*)\s+(chem_\w+)\s*\(", text, re.M)
+    return sorted(set(decl))
+
+
+def test_header_declarations_match_binding():
+    from paper_2510_23993_b200 import binding
+    assert sorted(binding.EXPORTED) == _declared()
+
+
+def test_library_exports_every_symbol():
+    from paper_2510_23993_b200 import binding, build
+    build.build()
+    lib = ctypes.CDLL(str(binding.LIB_PATH))
+    for name in _declared():
+        assert hasattr(lib, name), name
+    out = subprocess.run(["nm", "-D", "--defined-only", str(binding.LIB_PATH)], capture_output=True, text=True).stdout
+    for name in _declared():
+        assert re.search(rf"\bT {name}\b", out), name
+
+
+def test_library_is_sm100a_only():
+    from paper_2510_23993_b200 import binding
+    out = subprocess.run(["cuobjdump", "--list-elf", str(binding.LIB_PATH)], capture_output=True, text=True).stdout
+    arches = set(re.findall(r"sm_(\d+a?)", out))
+    assert arches == {"100a"}, arches
+
+
+def test_default_opts_are_the_papers():
+    from paper_2510_23993_b200 import binding
+    o = binding.default_opts()
+    assert (o.kmax_bulk, o.n_active_star, o.kmax_sparse, o.T_min) == (5, 10000, 100000, 500.0)
+
+
+def test_init_rejects_unbalanced_mechanism_without_gpu():
+    """chem_init validates before touching the device: an imbalanced row is CHEM_EMECH."""
+    from paper_2510_23993_b200 import binding, mechanism
+    lib = binding.load_library()
+    mt = mechanism.load("toy_a_to_b")
+    mt.nu_r[0, 1] = 2.0
+    d, keep = binding.mech_desc(mt)
+    h = ctypes.c_void_p()
+    assert lib.chem_init(ctypes.byref(d), None, 0, ctypes.byref(h)) == -2
+
+
+def test_init_unknown_structure_without_gpu():
+    from paper_2510_23993_b200 import binding, mechanism
+    lib = binding.load_library()
+    mt = mechanism.load("toy_a_to_b")
+    mt.reversible[0] = 1       # a reversible A<=>B with toy_a_to_b's numbers: valid, but the
+    mt.A[0] = 7.0              # structure (reversible row) matches toy_a_eq_b -> accepted...
+    d, keep = binding.mech_desc(mt)
+    h = ctypes.c_void_p()
+    rc = lib.chem_init(ctypes.byref(d), None, 0, ctypes.byref(h))
+    assert rc in (0, -4)       # -4: structure matched but no CUDA device in this container
+    mt.nu_f[0, 0] = 2.0        # 2A <=> 2B ... still balanced, no compiled structure
+    mt.nu_r[0, 1] = 2.0
+    d, keep = binding.mech_desc(mt)
+    assert lib.chem_init(ctypes.byref(d), None, 0, ctypes.byref(h)) == -3
+
+
+def test_product_does_not_import_oracle():
+    code = ("import sys, paper_2510_23993_b200 as p; from paper_2510_23993_b200 import binding, mechanism, "
+            "gen_structure, build; import paper_2510_23993_b200.api; "
+            "assert not any(m == 'oracle' or m.startswith('oracle.') for m in sys.modules), "
+            "[m for m in sys.modules if 'oracle' in m]")
+    subprocess.run([sys.executable, "-c", code], check=True, cwd=ROOT)
+
+
+def test_no_oracle_reference_in_product_sources():
+    for p in (ROOT / "paper_2510_23993_b200").rglob("*"):
+        if p.suffix in (".py", ".cu", ".cuh", ".h"):
+            txt = p.read_text()
+            assert "import oracle" not in txt and "from oracle" not in txt, p
+            assert "liboracle" not in txt, p

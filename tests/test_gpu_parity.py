@@ -1,0 +1,260 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element on the
+same seeded inputs (BASELINE.json north_star tolerances; SURVEY.md §8(c) readings 13-14):
+
+  * rates:      |Omega_gpu - Omega_ora| <= 1e-10 G_k (+1e-300), G_k the gross species rate,
+                and plain relative 1e-10 wherever |Omega_k| >= 1e-3 G_k;
+  * integration: T and Y_k (oracle Y_k > 1e-12) relative 1e-6 after one dt, GPU at the parity
+                tolerance rtol = 1e-9, atol_Y = 1e-20, atol_T = 1e-6 K; oracle at rtol 1e-12,
+                atol_Y 1e-24, atol_T 1e-9 K.
+"""
+import numpy as np
+import pytest
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from oracle import Oracle  # noqa: E402
+from paper_2510_23993_b200 import Chem  # noqa: E402
+
+DEV = torch.device("cuda", 0)
+RTOL_RATES = 1e-10
+RTOL_STATE = 1e-6
+GPU_TOL = dict(rtol=1e-9, atol=1e-20)
+ORA_TOL = dict(rtol=1e-12, atolY=1e-24, atolT=1e-9)
+
+
+@pytest.fixture(scope="module")
+def ora():
+    return Oracle("h2air_li2004")
+
+
+@pytest.fixture(scope="module")
+def chem():
+    return Chem("h2air_li2004", device=0, atol_T=1e-6)
+
+
+def to_dev(x):
+    return torch.as_tensor(np.ascontiguousarray(x), dtype=torch.float64, device=DEV)
+
+
+def species_dev(Y, pad=0):
+    """cell-major numpy [n, ns] -> component-major device [ns, n + pad] (ragged ld)."""
+    n, ns = Y.shape
+    out = torch.full((ns, n + pad), np.nan, dtype=torch.float64, device=DEV)
+    out[:, :n] = to_dev(Y.T)
+    return out
+
+
+def rates_close(w_gpu, w_ora, G):
+    ok = np.abs(w_gpu - w_ora) <= RTOL_RATES * G + 1e-300
+    big = np.abs(w_ora) >= 1e-3 * G
+    ok &= ~big | (np.abs(w_gpu - w_ora) <= RTOL_RATES * np.abs(w_ora))
+    return ok
+
+
+def test_structure(chem):
+    assert chem.structure == "h2air_li2004"
+
+
+def test_rates_parity_cfg1d(chem, ora):
+    m = ora.m
+    d = synth.cfg1d(m.species, m.W, n=3001)   # several tiles + a ragged tail
+    Yd = species_dev(d["Y"], pad=7)
+    w = chem.rates(to_dev(d["rho"]), to_dev(d["T"]), Yd).cpu().numpy()[:, :3001].T
+    for i in range(3001):
+        wo, qf, qr = ora.rates(d["rho"][i], d["T"][i], d["Y"][i])
+        G = np.abs(m.nu_r - m.nu_f).T.astype(float) @ (np.abs(qf) + np.abs(qr))
+        assert rates_close(w[i], wo, G).all(), (i, w[i], wo)
+
+
+def test_rates_edge_cases(chem, ora):
+    """Zero mass fractions (log 0 = -inf path), pure inert, a single species, NASA range edges."""
+    m = ora.m
+    ns = m.ns
+    Ys, Ts = [], []
+    for k in range(ns):
+        y = np.zeros(ns); y[k] = 1.0
+        Ys.append(y); Ts.append(1200.0)
+    y = np.zeros(ns); y[0] = 0.5; y[1] = 0.5
+    Ys += [y, y, y, y]
+    Ts += [999.999999, 1000.0, 1000.000001, 3400.0]
+    Y = np.array(Ys); T = np.array(Ts)
+    rho = synth.rho_ideal(synth.P_ATM, T, Y, m.W)
+    w = chem.rates(to_dev(rho), to_dev(T), species_dev(Y)).cpu().numpy().T
+    for i in range(len(T)):
+        wo, qf, qr = ora.rates(rho[i], T[i], Y[i])
+        G = np.abs(m.nu_r - m.nu_f).T.astype(float) @ (np.abs(qf) + np.abs(qr))
+        assert rates_close(w[i], wo, G).all(), i
+    # pure N2: exactly zero
+    assert np.all(w[ns - 1] == 0.0)
+
+
+def test_energy_temperature(chem, ora):
+    m = ora.m
+    d = synth.cfg1d(m.species, m.W, n=1000, seed=7)
+    Yd = species_dev(d["Y"])
+    e = chem.energy(to_dev(d["T"]), Yd).cpu().numpy()
+    eo = np.array([ora.energy(t, y) for t, y in zip(d["T"], d["Y"])])
+    assert np.max(np.abs(e - eo) / np.abs(eo).clip(1e3)) < 1e-12
+    T = to_dev(np.full(1000, 1500.0))
+    chem.temperature(to_dev(eo), Yd, T)
+    assert np.max(np.abs(T.cpu().numpy() - d["T"])) < 1e-8
+
+
+def test_rhs_and_jacobian(chem, ora):
+    m = ora.m
+    d = synth.cfg1d(m.species, m.W, n=256, seed=9)
+    Y = d["Y"] + 1e-8            # stay off the max(Y, 0) kink, where one-sided derivatives differ
+    Y /= Y.sum(1, keepdims=True)
+    rho, T = d["rho"], d["T"]
+    f = chem.rhs(to_dev(rho), to_dev(T), species_dev(Y)).cpu().numpy()
+    J = chem.jacobian(to_dev(rho), to_dev(T), species_dev(Y)).cpu().numpy()
+    for i in range(len(T)):
+        y = np.r_[Y[i], T[i]]
+        fo = ora.rhs(rho[i], y)
+        Jo = ora.jac(rho[i], y)
+        wo, qf, qr = ora.rates(rho[i], T[i], Y[i])
+        G = np.abs(m.nu_r - m.nu_f).T.astype(float) @ (np.abs(qf) + np.abs(qr))
+        Gf = np.r_[m.W * G / rho[i], abs(fo[-1]) + 1e-300]
+        assert np.all(np.abs(f[:, i] - fo) <= 1e-10 * Gf + 1e-300), i
+        scale = np.abs(Jo).max(axis=1) + 1e-300
+        err = np.abs(J[:, :, i] - Jo).max(axis=1) / scale
+        assert err.max() < 1e-8, (i, err)
+
+
+def _run_gpu(chem, rho, e, T0, Y, dt, pad=0, solid=None, **tol):
+    n = len(rho)
+    Td = to_dev(np.r_[T0, np.full(pad, np.nan)])[:n] if pad else to_dev(T0)
+    Yd = species_dev(Y, pad)
+    sd = None if solid is None else torch.as_tensor(solid, dtype=torch.uint8, device=DEV)
+    st = chem.integrate(to_dev(rho), to_dev(e), Td, Yd, dt, solid=sd, **(tol or GPU_TOL))
+    return Td.cpu().numpy(), Yd.cpu().numpy()[:, :n].T, st
+
+
+def _check_state(T, Y, out, label):
+    mask = out["Y"] > 1e-12
+    relY = np.abs(Y[mask] / out["Y"][mask] - 1)
+    relT = np.abs(T / out["T"] - 1)
+    assert relT.max() < RTOL_STATE, (label, relT.max())
+    assert relY.max() < RTOL_STATE, (label, relY.max())
+    return relT.max(), relY.max()
+
+
+@pytest.mark.parametrize("cfg", ["cfg1", "cfg1c"])
+def test_integrate_parity(chem, ora, cfg):
+    m = ora.m
+    d = getattr(synth, cfg)(m.species, m.W)
+    idx = np.arange(len(d["rho"])) if cfg == "cfg1" else np.arange(0, 4096, 16)   # 1c: 256 cells
+    rho, T0, Y = d["rho"][idx], d["T"][idx], d["Y"][idx]
+    e = np.array([ora.energy(t, y) for t, y in zip(T0, Y)])
+    out = ora.integrate_cells(rho, e, T0, Y, d["dt"], **ORA_TOL)
+    assert np.all(out["status"] == 0)
+    T, Yg, st = _run_gpu(chem, rho, e, T0, Y, d["dt"], pad=5)
+    assert st["n_unfinished"] == 0 and st["n_nonfinite"] == 0 and st["n_newton_fail"] == 0
+    _check_state(T, Yg, out, cfg)
+
+
+def test_gate_cold_solid_bitwise(chem, ora):
+    m = ora.m
+    d = synth.cfg1(m.species, m.W, n=300)
+    T0 = d["T"].copy()
+    T0[:50] = 300.0          # cold
+    solid = np.zeros(300, dtype=np.uint8)
+    solid[100:120] = 1
+    e = np.array([ora.energy(t, y) for t, y in zip(T0, d["Y"])])
+    Tg, Yg, st = _run_gpu(chem, d["rho"], e, T0, d["Y"], 1e-7, solid=solid)
+    untouched = np.r_[np.arange(50), np.arange(100, 120)]
+    assert np.array_equal(Tg[untouched], T0[untouched])
+    assert np.array_equal(Yg[untouched], d["Y"][untouched])
+    assert st["active0"] == 300 - 70
+
+
+def test_empty_and_all_cold(chem, ora):
+    m = ora.m
+    st = chem.integrate(to_dev(np.zeros(0)), to_dev(np.zeros(0)), to_dev(np.zeros(0)),
+                        torch.zeros((m.ns, 0), dtype=torch.float64, device=DEV), 1e-7)
+    assert st["cells"] == 0
+    d = synth.cfg1(m.species, m.W, n=64)
+    T0 = np.full(64, 300.0)
+    e = np.array([ora.energy(t, y) for t, y in zip(T0, d["Y"])])
+    Tg, Yg, st = _run_gpu(chem, d["rho"], e, T0, d["Y"], 1e-7)
+    assert st["active0"] == 0 and np.array_equal(Tg, T0) and np.array_equal(Yg, d["Y"])
+
+
+@pytest.mark.parametrize("mech,y0,t,exact", [
+    ("toy_a_to_b", [0.8, 0.2], 5e-3, lambda t: 0.8 * np.exp(-1e3 * t)),
+    ("toy_a_eq_b", [0.9, 0.1], 4e-3, lambda t: 0.5 + 0.4 * np.exp(-2e3 * t)),
+    ("toy_2a_to_b", [1.0, 0.0], 1e-2, lambda t: 1.0 / (1 + 2 * 10.0 * 50.0 * t)),
+])
+def test_closed_forms_gpu(mech, y0, t, exact):
+    """SURVEY §8(c) closed forms on the CUDA path (rtol 1e-11 -> 1e-8 relative)."""
+    ch = Chem(mech, device=0, atol_T=1e-9)
+    o = Oracle(mech)
+    n = 64
+    rho = np.full(n, 1.0)
+    T0 = np.full(n, 700.0)
+    Y = np.tile(np.array(y0, dtype=float), (n, 1))
+    e = np.array([o.energy(a, b) for a, b in zip(T0, Y)])
+    Td = to_dev(T0)
+    Yd = species_dev(Y)
+    ch.integrate(to_dev(rho), to_dev(e), Td, Yd, t, rtol=1e-11, atol=1e-20)
+    YA = Yd.cpu().numpy()[0]
+    assert np.max(np.abs(YA / exact(t) - 1)) < 1e-8
+    assert np.max(np.abs(Td.cpu().numpy() - 700.0)) < 1e-8
+
+
+def test_schedule_invariance_bitwise(chem, ora):
+    """P:177 / S:191: bulk-sparse == naive (Alg. 2) per cell, bitwise, for any K_max_bulk, N*,
+    compaction mode (P:181 index map vs all-cells launches)."""
+    m = ora.m
+    d = synth.cfg1c(m.species, m.W)
+    idx = np.arange(0, 4096, 8)
+    rho, T0, Y = d["rho"][idx], d["T"][idx], d["Y"][idx]
+    e = np.array([ora.energy(t, y) for t, y in zip(T0, Y)])
+    ref = None
+    configs = [dict(kmax_bulk=1 << 30, n_active_star=0),        # naive: one launch to t_final
+               dict(kmax_bulk=1, n_active_star=0),
+               dict(kmax_bulk=5, n_active_star=100),
+               dict(kmax_bulk=5, n_active_star=10 ** 9),       # sparse only
+               dict(kmax_bulk=3, n_active_star=50, compact_bulk=0)]
+    for cfgo in configs:
+        chem.set_opts(**{**dict(kmax_bulk=5, n_active_star=10000, compact_bulk=1), **cfgo})
+        T, Yg, st = _run_gpu(chem, rho, e, T0, Y, d["dt"])
+        if ref is None:
+            ref = (T, Yg, st["steps_attempted"])
+        else:
+            assert np.array_equal(T, ref[0]) and np.array_equal(Yg, ref[1]), cfgo
+            assert st["steps_attempted"] == ref[2]
+    chem.set_opts(kmax_bulk=5, n_active_star=10000, compact_bulk=1)
+
+
+def test_boxes_fused_equals_single(chem, ora):
+    """A10: one fused launch over several boxes (different dt, ld) == each box alone, bitwise."""
+    from paper_2510_23993_b200 import Box
+    m = ora.m
+    d = synth.cfg1c(m.species, m.W)
+    rng = np.random.default_rng(3)
+    sizes = [37, 200, 1, 64, 129]
+    dts = [1e-7, 1e-5, 1e-6, 3e-5, 2e-7]
+    boxes, singles = [], []
+    start = 0
+    for n, dt in zip(sizes, dts):
+        sel = rng.integers(0, 4096, n)
+        rho, T0, Y = d["rho"][sel], d["T"][sel], d["Y"][sel]
+        e = np.array([ora.energy(t, y) for t, y in zip(T0, Y)])
+        boxes.append(Box(to_dev(rho), to_dev(e), to_dev(T0), species_dev(Y, pad=3), dt))
+        singles.append(_run_gpu(chem, rho, e, T0, Y, dt, pad=3))
+        start += n
+    cost = torch.zeros(len(boxes), dtype=torch.float64, device=DEV)
+    st = chem.integrate_boxes(boxes, box_cost=cost, **GPU_TOL)
+    for bx, (T, Yg, s1) in zip(boxes, singles):
+        assert np.array_equal(bx.T.cpu().numpy(), T)
+        assert np.array_equal(bx.Y.cpu().numpy()[:, :bx.ncells].T, Yg)
+    c = cost.cpu().numpy()
+    assert np.isclose(c.sum(), st["steps_attempted"])
+    assert all(ci == s[2]["steps_attempted"] for ci, s in zip(c, singles))
