@@ -45,6 +45,7 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--cpu-sample-seconds", type=float, default=15.0)
+    p.add_argument("--balance", default="lpt", choices=["lpt", "none"])
     return p.parse_args()
 
 
@@ -99,28 +100,103 @@ class ClockSampler:
                 "power_w_max": max(pw) if pw else None, "samples": len(sm), "reasons": sorted(reasons)}
 
 
-# ------------------------------------------------------------------ field construction
-def build_field(args, chem, doc, device, rank):
-    import torch
-    import synth
+# ------------------------------------------------------------------ workloads
+class Workload:
+    """boxes (this rank's), the fused calls one step makes (lists of box indices), pristine inputs."""
+
+    def __init__(self, boxes, calls, meta, cell_steps, extra=None):
+        import torch
+        self.boxes, self.calls, self.meta = boxes, calls, meta
+        self.cell_steps = cell_steps                 # cell-steps this rank advances per step
+        self.pristine = [(b.T.clone(), b.Y.clone()) for b in boxes]
+        self.extra = extra or {}
+        torch.cuda.synchronize()
+
+    def restore(self):
+        for b, (T, Y) in zip(self.boxes, self.pristine):
+            b.T.copy_(T)
+            b.Y.copy_(Y)
+
+    def step(self, chem, rtol, atol, cost=None):
+        stats = []
+        for c in self.calls:
+            bx = [self.boxes[i] for i in c]
+            cc = None
+            if cost is not None:
+                import torch
+                cc = torch.zeros(len(c), dtype=torch.float64, device=self.boxes[0].rho.device)
+            stats.append(chem.integrate_boxes(bx, rtol=rtol, atol=atol, box_cost=cc))
+            if cost is not None:
+                cost[c] += cc.cpu().numpy()
+        return stats
+
+
+def _mk_boxes(chem, raw):
     from paper_2510_23993_b200 import Box
-    if args.config == "cfg2":
-        raw, meta = synth.field_cfg2(doc, device=device)
-    else:
-        raise SystemExit(f"unknown --config {args.config}")
-    boxes = []
+    out = []
     for b in raw:
         e = chem.energy(b["T"], b["Y"])            # e = u(T0, Y) with the CUDA path's own thermo
-        boxes.append(Box(b["rho"], e, b["T"].clone(), b["Y"].clone(), b["dt"], b.get("solid")))
-    pristine = [(b.T.clone(), b.Y.clone()) for b in boxes]
-    torch.cuda.synchronize()
-    return boxes, pristine, meta
+        out.append(Box(b["rho"], e, b["T"].clone(), b["Y"].clone(), b["dt"], b.get("solid")))
+    return out
 
 
-def restore(boxes, pristine):
-    for b, (T, Y) in zip(boxes, pristine):
-        b.T.copy_(T)
-        b.Y.copy_(Y)
+def build_workload(args, chem, doc, device, rank, world):
+    import synth
+    from paper_2510_23993_b200 import sharding
+    m = chem.mech
+    if args.config == "cfg2":
+        raw, meta = synth.field_cfg2(doc, device=device)
+        boxes = _mk_boxes(chem, raw)
+        return Workload(boxes, [list(range(len(boxes)))], meta, sum(b.ncells for b in boxes))
+    if args.config == "cfg3":
+        raw, meta = synth.field_cfg3(doc, m.W, m.species, device=device)
+        boxes = _mk_boxes(chem, raw)
+        return Workload(boxes, [list(range(len(boxes)))], meta, sum(b.ncells for b in boxes))
+    if args.config == "cfg5":
+        nb = 128
+        ids = list(range(rank, nb, world))         # strong split of one field over the ranks
+        raw, meta = synth.field_cfg5(doc, m.W, m.species, device=device, box_ids=ids)
+        boxes = _mk_boxes(chem, raw)
+        meta["scaling"] = "strong"
+        return Workload(boxes, [list(range(len(boxes)))], meta, sum(b.ncells for b in boxes))
+    if args.config == "cfg4":
+        # weak scaling: P copies of the 3-level hierarchy; copy p calibrated on rank p, then the
+        # P*192 boxes are redistributed by LPT on the measured per-box cost (SURVEY §8(e)).
+        import numpy as np
+        all_desc = [d for p in range(world) for d in synth.hierarchy_cfg4(copy=p)]
+        mine = [i for i, d in enumerate(all_desc) if d["copy"] == rank]
+
+        def calls_for(idx):
+            lv = [all_desc[i]["level"] for i in idx]
+            # one coarse step with subcycling (P:116): L0 x1 (dt), L1 x2 (dt/2), L2 x4 (dt/4),
+            # fused across levels: {L0,L1,L2}, {L1,L2}, {L2}, {L2}
+            return [[k for k, l in enumerate(lv) if l >= 0], [k for k, l in enumerate(lv) if l >= 1],
+                    [k for k, l in enumerate(lv) if l >= 2], [k for k, l in enumerate(lv) if l >= 2]]
+
+        raw = [synth.build_cfg4_box(doc, m.W, m.species, all_desc[i], device) for i in mine]
+        w0 = Workload(_mk_boxes(chem, raw), calls_for(mine), {}, 0)
+        cost = np.zeros(len(mine))
+        w0.step(chem, args.rtol, args.atol, cost=cost)
+        if world > 1 and args.balance == "lpt":
+            gcost, owner = sharding.balance(cost)
+        else:
+            gcost = np.concatenate([cost] * world) if world > 1 else cost
+            owner = np.array([d["copy"] for d in all_desc])
+        imb = sharding.imbalance(gcost, owner, world) if world > 1 else 1.0
+        own = [i for i in range(len(all_desc)) if owner[i] == rank]
+        if own == mine:
+            boxes = w0.boxes
+        else:
+            del w0
+            boxes = _mk_boxes(chem, [synth.build_cfg4_box(doc, m.W, m.species, all_desc[i], device) for i in own])
+        calls = calls_for(own)
+        cell_steps = sum(b.ncells * 2 ** all_desc[i]["level"] for b, i in zip(boxes, own))
+        meta = dict(workload=f"cfg4: 3-level AMR hierarchy (ratio 2, 32^3 boxes, 192 boxes/copy, 6.3M cells/copy) "
+                             f"of detonation fields, {world} copies, subcycled coarse step (4 fused calls), "
+                             f"balance={args.balance}", cells=sum(b.ncells for b in boxes))
+        return Workload(boxes, calls, meta, cell_steps, extra=dict(imbalance_max_over_mean=imb,
+                                                                   boxes_owned=len(own)))
+    raise SystemExit(f"unknown --config {args.config}")
 
 
 # ------------------------------------------------------------------ oracle (cpu baseline / reference arm)
@@ -155,6 +231,9 @@ def reference_arm(args):
         return
     import synth
     doc = synth.load_trajectories()
+    if args.config != "cfg2":
+        print(json.dumps({"impl": "reference", "unavailable": "reference arm implemented for cfg2 only"}))
+        return
     meta = _meta_cfg2(doc)
     times, cells = [], 0
     for i in range(args.warmup + args.steps):
@@ -185,6 +264,44 @@ def _meta_cfg2(doc):
 
 
 # ------------------------------------------------------------------ our arm
+def oracle_sample_field(wl, seconds_target, rtol, atol, T_min=500.0):
+    """cpu_baseline for a non-uniform field: the oracle on a random sample of the field's active
+    cells (each rank-0 box contributes), extrapolated to the field as n_active x (time per sampled
+    cell with all threads); gated cells cost nothing on either side.  Labelled an extrapolation."""
+    from oracle import Oracle
+    o = Oracle("h2air_li2004")
+    rng = np.random.default_rng(0)
+    cells, n_act = [], 0
+    for bi, (b, (T0, Y0)) in enumerate(zip(wl.boxes, wl.pristine)):
+        act = np.nonzero((T0 >= T_min).cpu().numpy())[0]
+        n_act += len(act)
+        for i in rng.choice(act, size=min(len(act), 64), replace=False) if len(act) else []:
+            cells.append((b.rho[i].item(), T0[i].item(), Y0[:, i].cpu().numpy(), b.dt))
+    rng.shuffle(cells)
+    nth = o.max_threads()
+
+    def run(sub):
+        rho = np.array([c[0] for c in sub]); T = np.array([c[1] for c in sub]); Y = np.array([c[2] for c in sub])
+        e = np.array([o.energy(t, y) for t, y in zip(T, Y)])
+        t0 = time.perf_counter()
+        for d in sorted(set(c[3] for c in sub)):
+            sel = np.array([c[3] == d for c in sub])
+            o.integrate_cells(rho[sel], e[sel], T[sel], Y[sel], d, rtol=rtol, atolY=atol, atolT=ATOL_T, nthreads=nth)
+        return time.perf_counter() - t0
+
+    n = min(len(cells), 4 * nth)
+    dt = run(cells[:n])
+    while dt < seconds_target / 4 and n < len(cells):
+        n = min(len(cells), n * 4)
+        dt = run(cells[:n])
+    per_cell = dt / n
+    total_cells = sum(b.ncells for b in wl.boxes)
+    value = total_cells / (n_act * per_cell) / 1e6
+    return dict(value=value, threads=nth, cells=n, seconds=dt, n_active=n_act,
+                sample=f"{n} random active cells of the {wl.meta['workload'][:5]} field timed on {nth} threads "
+                       f"({dt:.1f} s), extrapolated to the field's {n_act} active of {total_cells} cells")
+
+
 def ours(args):
     import torch
     import torch.distributed as dist
@@ -204,16 +321,13 @@ def ours(args):
     method = {"rodas4": 0, "rodas3": 1}[args.method]
     chem = Chem("h2air_li2004", device=local, atol_T=ATOL_T, method=method)
     doc = synth.load_trajectories()
-    boxes, pristine, meta = build_field(args, chem, doc, device, rank)
-    ncells = sum(b.ncells for b in boxes)
+    wl = build_workload(args, chem, doc, device, rank, world)
+    ncells = sum(b.ncells for b in wl.boxes)
     fm = FlopModel(chem.mech, stages=6 if method == 0 else 4)
 
-    def step():
-        return chem.integrate_boxes(boxes, rtol=args.rtol, atol=args.atol)
-
     for _ in range(args.warmup):
-        restore(boxes, pristine)
-        step()
+        wl.restore()
+        wl.step(chem, args.rtol, args.atol)
     torch.cuda.synchronize()
 
     clocks = ClockSampler(local)
@@ -224,9 +338,9 @@ def ours(args):
     torch.cuda.synchronize()
     clocks.start()
     for k in range(args.steps):
-        restore(boxes, pristine)                       # untimed: before the start event
+        wl.restore()                                   # untimed: before the start event
         ev[k][0].record()
-        stats.append(step())
+        stats += wl.step(chem, args.rtol, args.atol)
         ev[k][1].record()
     torch.cuda.synchronize()
     if world > 1:
@@ -234,18 +348,23 @@ def ours(args):
     clk = clocks.stop()
     step_ms = [a.elapsed_time(b) for a, b in ev]
     t_total = sum(step_ms) / 1e3
+    t_rank = t_total
+    tot_cs = wl.cell_steps
     if world > 1:
         t = torch.tensor([t_total], dtype=torch.float64, device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_total = float(t.item())
-    value = world * ncells * args.steps / t_total / 1e6
+        c = torch.tensor([float(wl.cell_steps)], dtype=torch.float64, device=device)
+        dist.all_reduce(c, op=dist.ReduceOp.SUM)
+        tot_cs = float(c.item())
+    value = tot_cs * args.steps / t_total / 1e6
 
     # roofline of the dominant kernel (k_integrate: bulk + sparse launches, CUDA-event timed by the
     # library on the launching stream)
     flops = sum(fm.flops(s) for s in stats)
     k_ms = sum(s["t_bulk_ms"] + s["t_sparse_ms"] for s in stats)
     launches_int = sum(s["bulk_iters"] + (1 if s["sparse_cells"] > 0 else 0) for s in stats)
-    achieved = flops / (k_ms / 1e3) / 1e12
+    achieved = flops / (k_ms / 1e3) / 1e12 if k_ms > 0 else 0.0
     sm_mhz_peak = 1965.0
     try:
         mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -255,12 +374,12 @@ def ours(args):
     peak = fp64_peak_tflops(sm_mhz=sm_mhz_peak)
     gpu_launches = sum(1 + 2 * s["bulk_iters"] + (1 if s["sparse_cells"] > 0 else 0) for s in stats)
 
-    # e2e through the public API with host buffers (H2D + call + D2H inside the timed region)
+    # e2e through the public API with host buffers (H2D + calls + D2H inside the timed region)
     e2e = None
     if not args.no_e2e:
         host = [dict(rho=b.rho.cpu().pin_memory(), e=b.e.cpu().pin_memory(), T=p[0].cpu().pin_memory(),
-                     Y=p[1].cpu().pin_memory(), dt=b.dt) for b, p in zip(boxes, pristine)]
-        hr = HostRunner(chem, host)
+                     Y=p[1].cpu().pin_memory(), dt=b.dt) for b, p in zip(wl.boxes, wl.pristine)]
+        hr = HostRunner(chem, host, wl.calls)
         hr.step(args.rtol, args.atol)
         torch.cuda.synchronize()
         e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -278,37 +397,46 @@ def ours(args):
             t = torch.tensor([te], dtype=torch.float64, device=device)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             te = float(t.item())
-        e2e = {"value": world * ncells * args.steps / te / 1e6, "unit": "Mcell-steps/s",
+        e2e = {"value": tot_cs * args.steps / te / 1e6, "unit": "Mcell-steps/s",
                "h2d_bytes_per_step": hr.h2d_bytes, "d2h_bytes_per_step": hr.d2h_bytes}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        r = oracle_sample(meta, args.cpu_sample_seconds, args.rtol, args.atol)
-        cpu = {"value": r["value"], "unit": "Mcell-steps/s", "cores": r["threads"], "kind": "oracle",
-               "sample": f"{r['cells']} cells of the {args.config} state (all cfg2 cells are identical), "
-                         f"{r['seconds']:.1f} s on {r['threads']} threads, same rtol/atol as the GPU run"}
+        if args.config == "cfg2":
+            r = oracle_sample(wl.meta, args.cpu_sample_seconds, args.rtol, args.atol)
+            cpu = {"value": r["value"], "unit": "Mcell-steps/s", "cores": r["threads"], "kind": "oracle",
+                   "sample": f"{r['cells']} cells of the cfg2 state (all cfg2 cells are identical), "
+                             f"{r['seconds']:.1f} s on {r['threads']} threads, same rtol/atol as the GPU run"}
+        else:
+            r = oracle_sample_field(wl, args.cpu_sample_seconds, args.rtol, args.atol)
+            cpu = {"value": r["value"], "unit": "Mcell-steps/s", "cores": r["threads"], "kind": "oracle",
+                   "sample": r["sample"], "extrapolated": True}
 
+    att = sum(s["steps_attempted"] for s in stats) / args.steps
+    acc = sum(s["steps_accepted"] for s in stats) / args.steps
     s0 = stats[-1]
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "Mcell-steps/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * t_total / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": meta["workload"], "cells_per_gpu": ncells, "boxes_per_gpu": len(boxes),
+            "scaling": wl.meta.get("scaling", "weak"), "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": wl.meta["workload"], "cells_per_gpu": ncells, "boxes_per_gpu": len(wl.boxes),
+                       "cell_steps_per_step_per_gpu": wl.cell_steps, "fused_calls_per_step": len(wl.calls),
                        "rtol": args.rtol, "atol_Y": args.atol, "atol_T": ATOL_T, "method": args.method,
-                       "l2": "inputs 369 MB/GPU > 126 MB L2 (no flush needed)", "parallelism": f"boxes x{world}"},
+                       "l2": "inputs >= 369 MB/GPU > 126 MB L2 (no flush needed)",
+                       "parallelism": f"boxes over {world} rank(s)", **wl.extra},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": None,
                          "kernel": "k_integrate (bulk+sparse)", "flops_per_step_model": fm.per_step(),
                          "peak_source": "148 SMs x 64 FP64 FMA/clk x 2 x sm_max_mhz (derived, DESIGN.md)"},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches, "clocks": clk,
-            "detail": {"step_ms": step_ms, "k_integrate_ms": k_ms / args.steps, "integrate_launches": launches_int,
-                       "substeps_per_cell": s0["steps_attempted"] / ncells,
-                       "accepted_per_cell": s0["steps_accepted"] / ncells, "bulk_iters": s0["bulk_iters"],
+            "detail": {"step_ms": step_ms, "rank0_seconds": t_rank, "k_integrate_ms": k_ms / args.steps,
+                       "integrate_launches": launches_int, "substeps_per_cell_step": att / max(wl.cell_steps, 1),
+                       "accepted_per_cell_step": acc / max(wl.cell_steps, 1), "bulk_iters": s0["bulk_iters"],
                        "active_per_iter": s0["active_per_iter"], "sparse_cells": s0["sparse_cells"],
-                       "t_gate_ms": s0["t_gate_ms"], "t_compact_ms": s0["t_compact_ms"],
-                       "n_unfinished": s0["n_unfinished"], "n_nonfinite": s0["n_nonfinite"],
-                       "max_energy_drift": s0["max_energy_drift"]},
+                       "active0": s0["active0"], "t_gate_ms": s0["t_gate_ms"], "t_compact_ms": s0["t_compact_ms"],
+                       "t_sparse_ms": s0["t_sparse_ms"], "n_unfinished": s0["n_unfinished"],
+                       "n_nonfinite": s0["n_nonfinite"], "max_energy_drift": s0["max_energy_drift"]},
         }
         print(json.dumps(line))
     if world > 1:

@@ -186,9 +186,10 @@ class HostRunner:
     """End-to-end public-API path for host-resident data (the bench's `e2e` leg): pinned host
     buffers -> H2D copies on the current stream -> chem_integrate_boxes -> D2H of (T, Y)."""
 
-    def __init__(self, chem: Chem, host_boxes):
+    def __init__(self, chem: Chem, host_boxes, calls=None):
         self.chem = chem
         self.host = host_boxes          # list of dict(rho, e, T, Y, dt) pinned CPU tensors
+        self.calls = calls or [list(range(len(host_boxes)))]
         dev = chem.device
         self.dev_boxes = [Box(torch.empty_like(h["rho"], device=dev), torch.empty_like(h["e"], device=dev),
                               torch.empty_like(h["T"], device=dev), torch.empty_like(h["Y"], device=dev), h["dt"])
@@ -204,7 +205,7 @@ class HostRunner:
             d.e.copy_(h["e"], non_blocking=True)
             d.T.copy_(h["T"], non_blocking=True)
             d.Y.copy_(h["Y"], non_blocking=True)
-        st = self.chem.integrate_boxes(self.dev_boxes, rtol=rtol, atol=atol)
+        st = [self.chem.integrate_boxes([self.dev_boxes[i] for i in c], rtol=rtol, atol=atol) for c in self.calls]
         for d, oT, oY in zip(self.dev_boxes, self.out_T, self.out_Y):
             oT.copy_(d.T, non_blocking=True)
             oY.copy_(d.Y, non_blocking=True)

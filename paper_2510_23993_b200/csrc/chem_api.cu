@@ -120,6 +120,9 @@ struct MechOps {
                 p.troe_iT3[r] = t[1] != 0.0 ? std::min(1.0 / t[1], 1e300) : 1e300;
                 p.troe_iT1[r] = t[2] != 0.0 ? std::min(1.0 / t[2], 1e300) : 1e300;
                 p.troe_T2[r] = t[3];
+                // Fc is exactly alpha in double for 1 K < T < 1e6 K when T*** <= 1e-20 and T* >= 1e20
+                p.troe_const[r] = (t[1] > 0.0 && t[1] <= 1e-20 && t[2] >= 1e20 && !(t[3] > 0.0)) ? 1 : 0;
+                p.troe_L[r] = std::log10(t[0]);
             }
             for (int i = 0; i < M::neff(r); ++i) p.effm1[M::eff_off(r) + i] = d->eff[r * ns + M::eff_sp(r, i)] - 1.0;
         }
@@ -167,16 +170,17 @@ struct MechOps {
         return cudaGetLastError();
     }
 
-    static constexpr size_t smem() { return (size_t)SmemLayout<M>::bytes_per_thread * kIntegrateBS; }
+    template <class Meth>
+    static constexpr size_t smem() { return (size_t)SmemLayout<M, Meth>::bytes_per_thread * kIntegrateBS; }
 
     template <class Meth>
     static cudaError_t launch(const P& p, const LaunchCtx& L, const uint32_t* ids, int64_t n, int kmax, int refill,
                               int fin, int grid, cudaStream_t s)
     {
         auto kern = k_integrate<M, Meth, kIntegrateBS>;
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem());
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem<Meth>());
         if (e != cudaSuccess) return e;
-        kern<<<grid, kIntegrateBS, smem(), s>>>(p, L, ids, n, kmax, refill, fin);
+        kern<<<grid, kIntegrateBS, smem<Meth>(), s>>>(p, L, ids, n, kmax, refill, fin);
         return cudaGetLastError();
     }
     static cudaError_t integrate(const void* pp, int method, const LaunchCtx& L, const uint32_t* ids, int64_t n,
@@ -191,8 +195,8 @@ struct MechOps {
     {
         int nb = 0;
         auto kern = k_integrate<M, Meth, kIntegrateBS>;
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem());
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kIntegrateBS, smem());
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem<Meth>());
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kIntegrateBS, smem<Meth>());
         return std::max(nb, 1);
     }
     static int blocks_per_sm(int method) { return method == CHEM_METHOD_RODAS3 ? bps<Rodas3>() : bps<Rodas4>(); }
@@ -214,7 +218,7 @@ struct MechOps {
         o.energy = &energy;
         o.integrate = &integrate;
         o.blocks_per_sm = &blocks_per_sm;
-        o.integrate_smem = smem();
+        o.integrate_smem = smem<Rodas4>();
         return o;
     }
 };

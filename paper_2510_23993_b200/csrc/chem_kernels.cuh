@@ -158,16 +158,22 @@ __global__ void __launch_bounds__(BS) k_box_cost(LaunchCtx L, const uint32_t* id
 // ----------------------------------------------------------------------------- A6/A7/A9 integrate
 // Per-thread shared memory: the n x n iteration matrix (I/(h gamma) - J, then its LU), an
 // n-vector scratch for the permuted right-hand side, and n pivot bytes.
-template <class M>
+// Per-thread shared memory (stride = block size, conflict-free): the n x n iteration matrix
+// (I/(h gamma) - J, then its LU), the S stage vectors K_s, and n pivot bytes.
+template <class M, class Meth>
 struct SmemLayout {
     static constexpr int n = M::NSA + 1;
-    static constexpr int doubles = n * n + n + (n + 7) / 8;
+    static constexpr int off_K = n * n;
+    static constexpr int off_piv = n * n + Meth::S * n;
+    static constexpr int doubles = off_piv + (n + 7) / 8;
     static constexpr int bytes_per_thread = doubles * 8;
 };
 
+// Per-thread event counters (32-bit: they stay in registers for the whole kernel; one Jacobian
+// and one LU per attempted step, so those two are derived from `attempted`).
 struct Counters {
-    unsigned long long attempted = 0, accepted = 0, rhs = 0, jac = 0, lu = 0, newton_fail = 0, nonfinite = 0,
-                       trange = 0, unfinished = 0, done = 0;
+    unsigned attempted = 0, accepted = 0, rhs = 0, newton_fail = 0, nonfinite = 0, trange = 0, unfinished = 0,
+             done = 0;
     double drift = 0.0;
 };
 
@@ -184,9 +190,11 @@ struct Cell {
 };
 
 // One attempted Rosenbrock substep on cell C (A6).  Returns 1 accepted, 0 rejected, -1 failure.
+// The stage loop is a runtime loop (one inlined copy of the RHS in the kernel: the fully
+// unrolled version overflowed the instruction cache); stage vectors live in shared memory.
 template <class M, class Meth>
 __device__ __forceinline__ int ros_step(const Params<M>& P, const LaunchCtx& L, Cell<M>& C, const SMat& A,
-                                        uint8_t* piv, int pstride, double* scratch, int sstride, Counters& cnt)
+                                        double* Ks, uint8_t* piv, int ss, Counters& cnt)
 {
     constexpr int n = M::NSA + 1;
     constexpr int S = Meth::S;
@@ -194,23 +202,21 @@ __device__ __forceinline__ int ros_step(const Params<M>& P, const LaunchCtx& L, 
     double f0[n];
     rhs_jac<M, false>(P, C.rho, C.y, C.Yin, f0, A);
     cnt.rhs++;
-    cnt.jac++;
-    double sc[n];
-#pragma unroll
-    for (int i = 0; i < n; ++i) sc[i] = ((i < M::NSA) ? L.atol : L.atolT) + L.rtol * fabs(C.y[i]);
     const double remaining = C.dt - C.t;
     if (!(C.h > 0.0)) {
-        // initial step: 1% of the time for y to change by its own size (Hairer-Norsett-Wanner
-        // I.II.4 d0/d1 heuristic), capped at dt; a frozen or equilibrated cell takes one step.
+        // initial step: 1% of the time for y to change by its own size (the d0/d1 heuristic of
+        // Hairer-Norsett-Wanner I, II.4), capped at dt.  A cell whose f moves y by < 1e-3
+        // tolerance units over the whole interval (frozen or equilibrated) takes h = dt at once.
         double d0 = 0.0, d1 = 0.0;
 #pragma unroll
         for (int i = 0; i < n; ++i) {
-            d0 = fma(C.y[i] / sc[i], C.y[i] / sc[i], d0);
-            d1 = fma(f0[i] / sc[i], f0[i] / sc[i], d1);
+            const double sc = ((i < M::NSA) ? L.atol : L.atolT) + L.rtol * fabs(C.y[i]);
+            d0 = fma(C.y[i] / sc, C.y[i] / sc, d0);
+            d1 = fma(f0[i] / sc, f0[i] / sc, d1);
         }
         d0 = sqrt(d0 / n);
         d1 = sqrt(d1 / n);
-        C.h = (d0 < 1e-5 || d1 < 1e-5) ? remaining : fmin(remaining, 0.01 * d0 / d1);
+        C.h = (d1 * remaining < 1e-3 || d0 < 1e-5) ? remaining : fmin(remaining, 0.01 * d0 / d1);
     }
     bool last = false;
     double h = C.h;
@@ -223,42 +229,51 @@ __device__ __forceinline__ int ros_step(const Params<M>& P, const LaunchCtx& L, 
     for (int i = 0; i < n; ++i)
 #pragma unroll
         for (int j = 0; j < n; ++j) A(i, j) = (i == j) ? ghinv - A(i, j) : -A(i, j);
-    const bool ok = lu_factor<n>(A, piv, pstride);
-    cnt.lu++;
+    const bool ok = lu_factor<n>(A, piv, ss);
 
-    double K[S][n];
     const double hinv = 1.0 / h;
-    static_for<0, S>([&](auto s_) {
-        constexpr int s = decltype(s_)::value;
-        double F[n];
-        if constexpr (s == 0 || !Meth::newf(s)) {
+    {   // stage 0: K_0 = A^{-1} f(y)
+        double x[n];
 #pragma unroll
-            for (int i = 0; i < n; ++i) F[i] = f0[i];
-        } else {
+        for (int i = 0; i < n; ++i) Ks[i * ss] = f0[i];
+        lu_solve<n>(A, piv, ss, Ks, ss, x);
+    }
+#pragma unroll 1
+    for (int s = 1; s < S; ++s) {
+        double F[n];
+        if (Meth::newf_rt(s)) {
             double ys[n];
 #pragma unroll
-            for (int i = 0; i < n; ++i) {
-                double v = C.y[i];
-                static_for<0, s>([&](auto j_) {
-                    constexpr int j = decltype(j_)::value;
-                    if constexpr (Meth::a(s, j) != 0.0) v = fma(Meth::a(s, j), K[j][i], v);
-                });
-                ys[i] = v;
+            for (int i = 0; i < n; ++i) ys[i] = C.y[i];
+#pragma unroll
+            for (int j = 0; j < S - 1; ++j) {
+                if (j < s) {
+                    const double a = Meth::a_rt(s, j);
+#pragma unroll
+                    for (int i = 0; i < n; ++i) ys[i] = fma(a, Ks[(j * n + i) * ss], ys[i]);
+                }
             }
             rhs<M>(P, C.rho, invrho, ys, C.Yin, F);
             cnt.rhs++;
+        } else {
+            // a_sj = 0 for all j (RODAS3 stage 1): the stage argument is y itself, f = f(y)
+#pragma unroll
+            for (int i = 0; i < n; ++i) F[i] = f0[i];
         }
 #pragma unroll
-        for (int i = 0; i < n; ++i) {
-            double v = F[i];
-            static_for<0, s>([&](auto j_) {
-                constexpr int j = decltype(j_)::value;
-                if constexpr (Meth::c(s, j) != 0.0) v = fma(Meth::c(s, j) * hinv, K[j][i], v);
-            });
-            K[s][i] = v;
+        for (int j = 0; j < S - 1; ++j) {
+            if (j < s) {
+                const double c = Meth::c_rt(s, j) * hinv;
+#pragma unroll
+                for (int i = 0; i < n; ++i) F[i] = fma(c, Ks[(j * n + i) * ss], F[i]);
+            }
         }
-        lu_solve<n>(A, piv, pstride, scratch, sstride, K[s]);
-    });
+        double* v = Ks + (s * n) * ss;
+#pragma unroll
+        for (int i = 0; i < n; ++i) v[i * ss] = F[i];
+        double x[n];
+        lu_solve<n>(A, piv, ss, v, ss, x);
+    }
 
     double ynew[n];
     double err = 0.0;
@@ -267,8 +282,9 @@ __device__ __forceinline__ int ros_step(const Params<M>& P, const LaunchCtx& L, 
         double v = C.y[i], ev = 0.0;
         static_for<0, S>([&](auto j_) {
             constexpr int j = decltype(j_)::value;
-            if constexpr (Meth::m(j) != 0.0) v = fma(Meth::m(j), K[j][i], v);
-            if constexpr (Meth::e(j) != 0.0) ev = fma(Meth::e(j), K[j][i], ev);
+            const double kj = Ks[(j * n + i) * ss];
+            if constexpr (Meth::m(j) != 0.0) v = fma(Meth::m(j), kj, v);
+            if constexpr (Meth::e(j) != 0.0) ev = fma(Meth::e(j), kj, ev);
         });
         ynew[i] = v;
         const double s = ((i < M::NSA) ? L.atol : L.atolT) + L.rtol * fmax(fabs(C.y[i]), fabs(v));
@@ -369,8 +385,8 @@ __device__ __forceinline__ void flush_counters(const LaunchCtx& L, Counters& c)
     warp_add(&L.stats[S_ATTEMPTED], c.attempted);
     warp_add(&L.stats[S_ACCEPTED], c.accepted);
     warp_add(&L.stats[S_RHS], c.rhs);
-    warp_add(&L.stats[S_JAC], c.jac);
-    warp_add(&L.stats[S_LU], c.lu);
+    warp_add(&L.stats[S_JAC], c.attempted);   // one Jacobian per attempted substep
+    warp_add(&L.stats[S_LU], c.attempted);    // one LU per attempted substep
     warp_add(&L.stats[S_NEWTON_FAIL], c.newton_fail);
     warp_add(&L.stats[S_NONFINITE], c.nonfinite);
     warp_add(&L.stats[S_TRANGE], c.trange);
@@ -396,11 +412,12 @@ __global__ void __launch_bounds__(BS) k_integrate(const __grid_constant__ Params
                                                   int refill, int final_phase)
 {
     extern __shared__ double smem[];
-    constexpr int n = M::NSA + 1;
+    using SL = SmemLayout<M, Meth>;
+    constexpr int n = SL::n;
     double* mine = smem + threadIdx.x;
     SMat A{mine, BS, n};
-    double* scratch = mine + n * n * BS;
-    uint8_t* piv = reinterpret_cast<uint8_t*>(smem + (n * n + n) * BS) + threadIdx.x;
+    double* Ks = mine + SL::off_K * BS;
+    uint8_t* piv = reinterpret_cast<uint8_t*>(smem + SL::off_piv * BS) + threadIdx.x;
 
     Counters cnt;
     Cell<M> C;
@@ -424,7 +441,7 @@ __global__ void __launch_bounds__(BS) k_integrate(const __grid_constant__ Params
             if (!ok) { L.state[g] = ST_FAILED; continue; }
             have = true;
         }
-        const int r = ros_step<M, Meth>(P, L, C, A, piv, BS, scratch, BS, cnt);
+        const int r = ros_step<M, Meth>(P, L, C, A, Ks, piv, BS, cnt);
         if (r < 0) {
             cnt.nonfinite++;
             store_cell<M>(P, L, C, ST_FAILED, cnt);
