@@ -109,6 +109,7 @@ typedef struct {
     int64_t sparse_cells;       /* cells handed to the sparse launch (Alg. 3 §3)                */
     int64_t steps_attempted;    /* substeps attempted (accepted + rejected), all cells          */
     int64_t steps_accepted;
+    int64_t steps_frozen;       /* first steps taken as one explicit step by frozen cells (subset of attempted) */
     int64_t rhs_evals, jac_evals, lu_count;
     int64_t n_unfinished;       /* cells with t < dt after the sparse launch (K_max exceeded)   */
     int64_t n_newton_fail;      /* temperature Newton not converged in 50 iterations            */

@@ -52,7 +52,7 @@ class ChemBox(ctypes.Structure):
 
 class ChemStats(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int64) for n in (
-        "cells", "active0", "bulk_iters", "sparse_cells", "steps_attempted", "steps_accepted", "rhs_evals",
+        "cells", "active0", "bulk_iters", "sparse_cells", "steps_attempted", "steps_accepted", "steps_frozen", "rhs_evals",
         "jac_evals", "lu_count", "n_unfinished", "n_newton_fail", "n_nonfinite", "n_T_range")] + [
         (n, ctypes.c_double) for n in ("t_gate_ms", "t_bulk_ms", "t_compact_ms", "t_sparse_ms",
                                        "max_energy_drift")] + [("active_per_iter", ctypes.c_int64 * 16)]

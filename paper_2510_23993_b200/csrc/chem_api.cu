@@ -637,6 +637,7 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
     const unsigned long long* hs = c->h_stats;
     st.steps_attempted = (int64_t)hs[S_ATTEMPTED];
     st.steps_accepted = (int64_t)hs[S_ACCEPTED];
+    st.steps_frozen = (int64_t)hs[S_FROZEN];
     st.rhs_evals = (int64_t)hs[S_RHS];
     st.jac_evals = (int64_t)hs[S_JAC];
     st.lu_count = (int64_t)hs[S_LU];

@@ -27,7 +27,7 @@ enum CellState : uint8_t {
 
 enum StatIdx {
     S_ATTEMPTED = 0, S_ACCEPTED, S_RHS, S_JAC, S_LU, S_NEWTON_FAIL, S_NONFINITE, S_TRANGE, S_UNFINISHED,
-    S_DONE, S_DRIFT_BITS, S_COUNT_ACTIVE, S_CURSOR, S_NSTATS
+    S_DONE, S_DRIFT_BITS, S_COUNT_ACTIVE, S_CURSOR, S_FROZEN, S_NSTATS
 };
 
 struct DevBox {
@@ -173,7 +173,7 @@ struct SmemLayout {
 // and one LU per attempted step, so those two are derived from `attempted`).
 struct Counters {
     unsigned attempted = 0, accepted = 0, rhs = 0, newton_fail = 0, nonfinite = 0, trange = 0, unfinished = 0,
-             done = 0;
+             done = 0, frozen = 0;
     double drift = 0.0;
 };
 
@@ -205,8 +205,7 @@ __device__ __forceinline__ int ros_step(const Params<M>& P, const LaunchCtx& L, 
     const double remaining = C.dt - C.t;
     if (!(C.h > 0.0)) {
         // initial step: 1% of the time for y to change by its own size (the d0/d1 heuristic of
-        // Hairer-Norsett-Wanner I, II.4), capped at dt.  A cell whose f moves y by < 1e-3
-        // tolerance units over the whole interval (frozen or equilibrated) takes h = dt at once.
+        // Hairer-Norsett-Wanner I, II.4), capped at dt.
         double d0 = 0.0, d1 = 0.0;
 #pragma unroll
         for (int i = 0; i < n; ++i) {
@@ -216,7 +215,20 @@ __device__ __forceinline__ int ros_step(const Params<M>& P, const LaunchCtx& L, 
         }
         d0 = sqrt(d0 / n);
         d1 = sqrt(d1 / n);
-        C.h = (d1 * remaining < 1e-3 || d0 < 1e-5) ? remaining : fmin(remaining, 0.01 * d0 / d1);
+        if (d1 * remaining < 1e-3) {
+            // frozen / inert / equilibrated cell (the north_star's "cheap bulk step"): f moves y by
+            // < 1e-3 tolerance units over the whole interval, so one explicit step y += dt f(y)
+            // is within that bound by construction; skip the LU and the stages.
+#pragma unroll
+            for (int i = 0; i < n; ++i) C.y[i] = fma(remaining, f0[i], C.y[i]);
+            C.t = C.dt;
+            C.k++;
+            cnt.attempted++;
+            cnt.accepted++;
+            cnt.frozen++;
+            return 1;
+        }
+        C.h = (d0 < 1e-5) ? remaining : fmin(remaining, 0.01 * d0 / d1);
     }
     bool last = false;
     double h = C.h;
@@ -385,8 +397,9 @@ __device__ __forceinline__ void flush_counters(const LaunchCtx& L, Counters& c)
     warp_add(&L.stats[S_ATTEMPTED], c.attempted);
     warp_add(&L.stats[S_ACCEPTED], c.accepted);
     warp_add(&L.stats[S_RHS], c.rhs);
-    warp_add(&L.stats[S_JAC], c.attempted);   // one Jacobian per attempted substep
-    warp_add(&L.stats[S_LU], c.attempted);    // one LU per attempted substep
+    warp_add(&L.stats[S_JAC], c.attempted);              // one Jacobian per attempted substep
+    warp_add(&L.stats[S_LU], c.attempted - c.frozen);    // one LU per attempted Rosenbrock substep
+    warp_add(&L.stats[S_FROZEN], c.frozen);
     warp_add(&L.stats[S_NEWTON_FAIL], c.newton_fail);
     warp_add(&L.stats[S_NONFINITE], c.nonfinite);
     warp_add(&L.stats[S_TRANGE], c.trange);

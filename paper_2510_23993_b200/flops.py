@@ -55,7 +55,7 @@ class FlopModel:
 
     def flops(self, stats):
         """Algorithmic FLOPs of one chem_integrate call from its chem_stats counters."""
-        att = stats["steps_attempted"]
+        att = stats["steps_attempted"] - stats.get("steps_frozen", 0)   # frozen steps: RHS + J, no LU/solves
         return (stats["rhs_evals"] * self.rhs + stats["jac_evals"] * self.jac + stats["lu_count"] * self.lu
                 + att * (self.stages * self.solve + self.control))
 
