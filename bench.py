@@ -46,6 +46,7 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--cpu-sample-seconds", type=float, default=15.0)
     p.add_argument("--balance", default="lpt", choices=["lpt", "none"])
+    p.add_argument("--lanes", type=int, default=1, choices=[1, 4, 8], help="lanes per cell (1: thread per cell)")
     return p.parse_args()
 
 
@@ -319,7 +320,7 @@ def ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=device)
     method = {"rodas4": 0, "rodas3": 1}[args.method]
-    chem = Chem("h2air_li2004", device=local, atol_T=ATOL_T, method=method)
+    chem = Chem("h2air_li2004", device=local, atol_T=ATOL_T, method=method, lanes_per_cell=args.lanes)
     doc = synth.load_trajectories()
     wl = build_workload(args, chem, doc, device, rank, world)
     ncells = sum(b.ncells for b in wl.boxes)
@@ -423,6 +424,7 @@ def ours(args):
             "config": {"workload": wl.meta["workload"], "cells_per_gpu": ncells, "boxes_per_gpu": len(wl.boxes),
                        "cell_steps_per_step_per_gpu": wl.cell_steps, "fused_calls_per_step": len(wl.calls),
                        "rtol": args.rtol, "atol_Y": args.atol, "atol_T": ATOL_T, "method": args.method,
+                       "lanes_per_cell": args.lanes,
                        "l2": "inputs >= 369 MB/GPU > 126 MB L2 (no flush needed)",
                        "parallelism": f"boxes over {world} rank(s)", **wl.extra},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",

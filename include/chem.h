@@ -85,9 +85,11 @@ typedef struct {
     int32_t method;         /* CHEM_METHOD_*                                                      */
     int32_t compact_bulk;   /* 1 (default): bulk bursts run over the compacted active list;
                                0: every bulk launch spans all cells of all boxes (paper's Alg. 3) */
+    int32_t lanes_per_cell; /* 1: one thread integrates one cell; 4 or 8: a lane group shares one
+                               cell (same mathematics, cooperative RHS/LU/solves) */
 } chem_opts;
 
-/* fills the paper's defaults: 500 K, 5, 1e4, 1e5, 1e-6 K, RODAS4, compact_bulk = 1 */
+/* fills the paper's defaults: 500 K, 5, 1e4, 1e5, 1e-6 K, RODAS4, compact_bulk = 1, lanes_per_cell = 1 */
 void chem_default_opts(chem_opts* o);
 
 /* ---- one AMR box / grid (FAB analogue) for the fused multi-box call ----------------- */

@@ -5,12 +5,13 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
 
 #include "../../include/chem.h"
-#include "chem_kernels.cuh"
+#include "chem_group.cuh"
 
 using namespace chem;
 
@@ -19,6 +20,7 @@ namespace {
 constexpr int kIntegrateBS = 64;   // threads per block of k_integrate (per-thread smem ~0.7 KB)
 constexpr int kStreamBS = 256;     // gate / compaction / box cost
 constexpr int kPointBS = 128;      // point kernels
+struct MechOpsBS { static constexpr int kGrp = 128; };   // threads per block of k_integrate_grp
 
 // ------------------------------------------------------------------ per-structure operations
 struct Ops {
@@ -38,7 +40,12 @@ struct Ops {
     cudaError_t (*energy)(const void*, int64_t, int64_t, const double*, const double*, double*, cudaStream_t);
     cudaError_t (*integrate)(const void*, int method, const LaunchCtx&, const uint32_t*, int64_t, int, int, int,
                              int grid, cudaStream_t);
+    cudaError_t (*integrate_grp)(const void* gtab, int method, int lanes, const LaunchCtx&, const uint32_t*, int64_t,
+                                 int, int, int, int grid, cudaStream_t);
     int (*blocks_per_sm)(int method);
+    int (*grp_blocks_per_sm)(int method, int lanes);
+    size_t gtab_size;
+    void (*build_gtab)(const void* params, void* out);
     size_t integrate_smem;
 };
 
@@ -134,7 +141,16 @@ struct MechOps {
                              const double* Y, double* w, cudaStream_t s)
     {
         if (n == 0) return cudaSuccess;
-        k_rates<M><<<grid_for(n, kPointBS), kPointBS, 0, s>>>(*static_cast<const P*>(pp), n, ld, rho, T, Y, w);
+        static const int minb = [] { const char* e = getenv("CHEM_RATES_MINB"); return e ? atoi(e) : 1; }();
+        const P& p = *static_cast<const P*>(pp);
+        const int g = grid_for(n, kPointBS);
+        switch (minb) {   // experiment hook: occupancy vs registers (not part of the ABI)
+        case 2: k_rates<M, 2><<<g, kPointBS, 0, s>>>(p, n, ld, rho, T, Y, w); break;
+        case 3: k_rates<M, 3><<<g, kPointBS, 0, s>>>(p, n, ld, rho, T, Y, w); break;
+        case 4: k_rates<M, 4><<<g, kPointBS, 0, s>>>(p, n, ld, rho, T, Y, w); break;
+        case 6: k_rates<M, 6><<<g, kPointBS, 0, s>>>(p, n, ld, rho, T, Y, w); break;
+        default: k_rates<M, 1><<<g, kPointBS, 0, s>>>(p, n, ld, rho, T, Y, w); break;
+        }
         return cudaGetLastError();
     }
     static cudaError_t rhs(const void* pp, int64_t n, int64_t ld, const double* rho, const double* T,
@@ -201,6 +217,48 @@ struct MechOps {
     }
     static int blocks_per_sm(int method) { return method == CHEM_METHOD_RODAS3 ? bps<Rodas3>() : bps<Rodas4>(); }
 
+    // ---- lane-group kernel
+    static constexpr int kGrpBS = MechOpsBS::kGrp;
+    template <class Meth, int G>
+    static cudaError_t launch_grp(const void* gt, const LaunchCtx& L, const uint32_t* ids, int64_t n, int kmax,
+                                  int refill, int fin, int grid, cudaStream_t s)
+    {
+        auto kern = k_integrate_grp<M, Meth, G, kGrpBS>;
+        const size_t sm = grp_smem_bytes<M, G>(kGrpBS);
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        if (e != cudaSuccess) return e;
+        kern<<<grid, kGrpBS, sm, s>>>(static_cast<const GTable<M>*>(gt), L, ids, n, kmax, refill, fin);
+        return cudaGetLastError();
+    }
+    static cudaError_t integrate_grp(const void* gt, int method, int lanes, const LaunchCtx& L, const uint32_t* ids,
+                                     int64_t n, int kmax, int refill, int fin, int grid, cudaStream_t s)
+    {
+        if (method == CHEM_METHOD_RODAS3)
+            return lanes == 4 ? launch_grp<Rodas3, 4>(gt, L, ids, n, kmax, refill, fin, grid, s)
+                              : launch_grp<Rodas3, 8>(gt, L, ids, n, kmax, refill, fin, grid, s);
+        return lanes == 4 ? launch_grp<Rodas4, 4>(gt, L, ids, n, kmax, refill, fin, grid, s)
+                          : launch_grp<Rodas4, 8>(gt, L, ids, n, kmax, refill, fin, grid, s);
+    }
+    template <class Meth, int G>
+    static int gbps()
+    {
+        int nb = 0;
+        auto kern = k_integrate_grp<M, Meth, G, kGrpBS>;
+        const size_t sm = grp_smem_bytes<M, G>(kGrpBS);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kGrpBS, sm);
+        return std::max(nb, 1);
+    }
+    static int grp_blocks_per_sm(int method, int lanes)
+    {
+        if (method == CHEM_METHOD_RODAS3) return lanes == 4 ? gbps<Rodas3, 4>() : gbps<Rodas3, 8>();
+        return lanes == 4 ? gbps<Rodas4, 4>() : gbps<Rodas4, 8>();
+    }
+    static void build_gtab(const void* params, void* out)
+    {
+        GTable<M>::build(*static_cast<const P*>(params), *static_cast<GTable<M>*>(out));
+    }
+
     static Ops ops()
     {
         Ops o;
@@ -218,6 +276,10 @@ struct MechOps {
         o.energy = &energy;
         o.integrate = &integrate;
         o.blocks_per_sm = &blocks_per_sm;
+        o.integrate_grp = &integrate_grp;
+        o.grp_blocks_per_sm = &grp_blocks_per_sm;
+        o.gtab_size = sizeof(GTable<M>);
+        o.build_gtab = &build_gtab;
         o.integrate_smem = smem<Rodas4>();
         return o;
     }
@@ -313,6 +375,8 @@ struct chem_ctx {
     int64_t* h_start = nullptr;       // pinned
     unsigned long long* h_stats = nullptr;  // pinned [S_NSTATS]
     cudaEvent_t ev[2] = {nullptr, nullptr};
+    void* d_gtab = nullptr;          // device copy of the lane-group kernel's table
+    bool grp_ok = false;             // the group kernel needs one shared NASA T_mid
 };
 
 namespace {
@@ -360,6 +424,7 @@ void chem_default_opts(chem_opts* o)
     o->atol_T = 1e-6;
     o->method = CHEM_METHOD_RODAS4;
     o->compact_bulk = 1;
+    o->lanes_per_cell = 1;
 }
 
 const char* chem_strerror(int code)
@@ -378,7 +443,8 @@ const char* chem_strerror(int code)
 static int check_opts(const chem_opts* o)
 {
     if (o->kmax_bulk < 1 || o->kmax_sparse < 1 || o->n_active_star < 0 || !(o->atol_T > 0.0) ||
-        (o->method != CHEM_METHOD_RODAS4 && o->method != CHEM_METHOD_RODAS3) || !std::isfinite(o->T_min))
+        (o->method != CHEM_METHOD_RODAS4 && o->method != CHEM_METHOD_RODAS3) || !std::isfinite(o->T_min) ||
+        (o->lanes_per_cell != 1 && o->lanes_per_cell != 4 && o->lanes_per_cell != 8))
         return CHEM_EINVAL;
     return CHEM_OK;
 }
@@ -405,6 +471,17 @@ int chem_init(const chem_mech_desc* mech, const chem_opts* opts, int device, che
     c->opts = o;
     c->params.resize(ops->params_size);
     ops->fill(mech, c->params.data());
+    c->grp_ok = true;
+    for (int k = 1; k < mech->ns; ++k) c->grp_ok = c->grp_ok && mech->T_range[3 * k + 1] == mech->T_range[1];
+    {
+        std::vector<unsigned char> gt(ops->gtab_size);
+        ops->build_gtab(c->params.data(), gt.data());
+        if (cudaMalloc(&c->d_gtab, ops->gtab_size) != cudaSuccess ||
+            cudaMemcpy(c->d_gtab, gt.data(), ops->gtab_size, cudaMemcpyHostToDevice) != cudaSuccess) {
+            delete c;
+            return CHEM_ECUDA;
+        }
+    }
     cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
     if (cudaMallocHost(&c->h_stats, sizeof(unsigned long long) * S_NSTATS) != cudaSuccess ||
         cudaEventCreate(&c->ev[0]) != cudaSuccess || cudaEventCreate(&c->ev[1]) != cudaSuccess ||
@@ -425,6 +502,7 @@ void chem_finalize(chem_ctx* c)
     if (c->h_stats) cudaFreeHost(c->h_stats);
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
+    if (c->d_gtab) cudaFree(c->d_gtab);
     delete c;
 }
 
@@ -580,6 +658,8 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
         return r;
     };
 
+    const bool use_grp = o.lanes_per_cell > 1 && c->grp_ok;
+
     // ---- Alg. 3 §1: gate + count + index map
     CK(cudaEventRecord(c->ev[0], s));
     k_gate<kStreamBS><<<grid_for(total, kStreamBS), kStreamBS, 0, s>>>(L, ids0);
@@ -599,8 +679,12 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
         const uint32_t* lst = all_cells ? nullptr : cur;
         const int64_t nl = all_cells ? total : n_cur;
         CK(cudaEventRecord(c->ev[0], s));
-        CK(ops.integrate(c->params.data(), o.method, L, lst, nl, o.kmax_bulk, 0, 0,
-                         (int)((nl + kIntegrateBS - 1) / kIntegrateBS), s));
+        if (use_grp)
+            CK(ops.integrate_grp(c->d_gtab, o.method, o.lanes_per_cell, L, lst, nl, o.kmax_bulk, 0, 0,
+                                 (int)((nl * o.lanes_per_cell + MechOpsBS::kGrp - 1) / MechOpsBS::kGrp), s));
+        else
+            CK(ops.integrate(c->params.data(), o.method, L, lst, nl, o.kmax_bulk, 0, 0,
+                             (int)((nl + kIntegrateBS - 1) / kIntegrateBS), s));
         CK(cudaEventRecord(c->ev[1], s));
         CK(cudaEventSynchronize(c->ev[1]));
         st.t_bulk_ms += elapsed(c);
@@ -620,11 +704,18 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
     // ---- Alg. 3 §3: sparse integration over the index map (persistent, lane refill)
     st.sparse_cells = n_cur;
     if (n_cur > 0) {
-        const int grid = std::max(1, std::min<int>(c->num_sms * ops.blocks_per_sm(o.method),
-                                                   (int)((n_cur + kIntegrateBS - 1) / kIntegrateBS)));
         CK(cudaMemsetAsync(L.stats + S_CURSOR, 0, 8, s));
         CK(cudaEventRecord(c->ev[0], s));
-        CK(ops.integrate(c->params.data(), o.method, L, cur, n_cur, o.kmax_sparse, 1, 1, grid, s));
+        if (use_grp) {
+            const int cells_per_block = MechOpsBS::kGrp / o.lanes_per_cell;
+            const int grid = std::max(1, std::min<int>(c->num_sms * ops.grp_blocks_per_sm(o.method, o.lanes_per_cell),
+                                                       (int)((n_cur + cells_per_block - 1) / cells_per_block)));
+            CK(ops.integrate_grp(c->d_gtab, o.method, o.lanes_per_cell, L, cur, n_cur, o.kmax_sparse, 1, 1, grid, s));
+        } else {
+            const int grid = std::max(1, std::min<int>(c->num_sms * ops.blocks_per_sm(o.method),
+                                                       (int)((n_cur + kIntegrateBS - 1) / kIntegrateBS)));
+            CK(ops.integrate(c->params.data(), o.method, L, cur, n_cur, o.kmax_sparse, 1, 1, grid, s));
+        }
         CK(cudaEventRecord(c->ev[1], s));
     }
     if (box_cost && n_active > 0) {

@@ -472,8 +472,9 @@ __global__ void __launch_bounds__(BS) k_integrate(const __grid_constant__ Params
 }
 
 // ----------------------------------------------------------------------------- point kernels
-template <class M>
-__global__ void k_rates(const __grid_constant__ Params<M> P, int64_t n, int64_t ld, const double* __restrict__ rho,
+template <class M, int MINB = 1>
+__global__ void __launch_bounds__(128, MINB) k_rates(const __grid_constant__ Params<M> P, int64_t n, int64_t ld,
+                                                    const double* __restrict__ rho,
                         const double* __restrict__ T, const double* __restrict__ Y, double* __restrict__ wdot)
 {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {

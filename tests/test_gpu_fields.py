@@ -111,7 +111,9 @@ def test_cfg2_full_size(chem, ora, doc):
     assert np.allclose(c, c[0]) and np.isclose(c.sum(), st["steps_attempted"])
 
 
-def test_cfg3_full_size(chem, ora, doc):
+@pytest.mark.parametrize("lanes", [1, 8])
+def test_cfg3_full_size(ora, doc, lanes):
+    chem = Chem("h2air_li2004", device=0, atol_T=1e-6, lanes_per_cell=lanes)
     m = ora.m
     raw, meta = synth.field_cfg3(doc, m.W, m.species, device=DEV)
     n_act = sum(int((r["T"] >= 500).sum()) for r in raw)

@@ -33,9 +33,10 @@ def ora():
     return Oracle("h2air_li2004")
 
 
-@pytest.fixture(scope="module")
-def chem():
-    return Chem("h2air_li2004", device=0, atol_T=1e-6)
+@pytest.fixture(scope="module", params=[1, 8, 4], ids=["lanes1", "lanes8", "lanes4"])
+def chem(request):
+    """Both integrator kernels: one thread per cell, and lane groups of 8 / 4 per cell."""
+    return Chem("h2air_li2004", device=0, atol_T=1e-6, lanes_per_cell=request.param)
 
 
 def to_dev(x):
@@ -186,14 +187,15 @@ def test_empty_and_all_cold(chem, ora):
     assert st["active0"] == 0 and np.array_equal(Tg, T0) and np.array_equal(Yg, d["Y"])
 
 
+@pytest.mark.parametrize("lanes", [1, 8])
 @pytest.mark.parametrize("mech,y0,t,exact", [
     ("toy_a_to_b", [0.8, 0.2], 5e-3, lambda t: 0.8 * np.exp(-1e3 * t)),
     ("toy_a_eq_b", [0.9, 0.1], 4e-3, lambda t: 0.5 + 0.4 * np.exp(-2e3 * t)),
     ("toy_2a_to_b", [1.0, 0.0], 1e-2, lambda t: 1.0 / (1 + 2 * 10.0 * 50.0 * t)),
 ])
-def test_closed_forms_gpu(mech, y0, t, exact):
+def test_closed_forms_gpu(mech, y0, t, exact, lanes):
     """SURVEY §8(c) closed forms on the CUDA path (rtol 1e-11 -> 1e-8 relative)."""
-    ch = Chem(mech, device=0, atol_T=1e-9)
+    ch = Chem(mech, device=0, atol_T=1e-9, lanes_per_cell=lanes)
     o = Oracle(mech)
     n = 64
     rho = np.full(n, 1.0)
@@ -224,6 +226,7 @@ def test_schedule_invariance_bitwise(chem, ora):
                dict(kmax_bulk=3, n_active_star=50, compact_bulk=0)]
     for cfgo in configs:
         chem.set_opts(**{**dict(kmax_bulk=5, n_active_star=10000, compact_bulk=1), **cfgo})
+        assert chem.opts.lanes_per_cell in (1, 4, 8)
         T, Yg, st = _run_gpu(chem, rho, e, T0, Y, d["dt"])
         if ref is None:
             ref = (T, Yg, st["steps_attempted"])
