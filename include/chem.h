@@ -75,6 +75,9 @@ typedef struct {
 /* ---- options ------------------------------------------------------------------------------ */
 #define CHEM_METHOD_RODAS4 0   /* 6-stage order-4 L-stable Rosenbrock, embedded order 3 (default) */
 #define CHEM_METHOD_RODAS3 1   /* 4-stage order-3 L-stable Rosenbrock, embedded order 2           */
+#define CHEM_METHOD_EXPLICIT 2 /* the paper's explicit 1st-order adaptive scheme: dt limited so
+                                  no Y_k (> 1e-12) changes by more than eps_change of itself; Euler
+                                  update clipped at 0; T from Newton every step    */
 
 typedef struct {
     double T_min;           /* gate T_reaction_min (value unstated -> 500 K) */
@@ -87,9 +90,11 @@ typedef struct {
                                0: every bulk launch spans all cells of all boxes (paper's Alg. 3) */
     int32_t lanes_per_cell; /* 1: one thread integrates one cell; 4 or 8: a lane group shares one
                                cell (same mathematics, cooperative RHS/LU/solves) */
+    double eps_change;      /* CHEM_METHOD_EXPLICIT: max fractional change per step (0.01; P:96 1-5%) */
 } chem_opts;
 
-/* fills the paper's defaults: 500 K, 5, 1e4, 1e5, 1e-6 K, RODAS4, compact_bulk = 1, lanes_per_cell = 1 */
+/* fills the paper's defaults: 500 K, 5, 1e4, 1e5, 1e-6 K, RODAS4, compact_bulk = 1, lanes_per_cell = 1,
+   eps_change = 0.01 */
 void chem_default_opts(chem_opts* o);
 
 /* ---- one AMR box / grid (FAB analogue) for the fused multi-box call ----------------- */

@@ -85,6 +85,8 @@ def _load():
         lib.or_integrate_cells.argtypes = [P, ctypes.c_int64, P, P, P, P, P, D, D, D, D, D,
                                            ctypes.c_int, P, P, P]
         lib.or_max_threads.restype = ctypes.c_int
+        lib.or_explicit_cells.argtypes = [P, ctypes.c_int64, P, P, P, P, P, D, D, D, ctypes.c_int64, ctypes.c_int,
+                                          P, P]
         _lib = lib
     return _lib
 
@@ -187,6 +189,21 @@ class Oracle:
         self.lib.or_integrate_cells(self._sp, n, _ptr(rho), _ptr(e), _ptr(T), _ptr(Y), _ptr(sol), float(dt),
                                     rtol, atolY, atolT, T_min, int(nth), _ptr(nst), _ptr(status), _ptr(T_int))
         return dict(T=T, Y=Y, status=status, nsteps=nst, T_int=T_int, threads=nth)
+
+    def explicit_cells(self, rho, e, T, Y, dt, eps=0.01, T_min=500.0, kmax=100000, solid=None, nthreads=None):
+        """The paper's explicit scheme over cell-major Y [n, ns]."""
+        n = len(rho)
+        rho = np.ascontiguousarray(rho, dtype=np.float64)
+        e = np.ascontiguousarray(e, dtype=np.float64)
+        T = np.array(T, dtype=np.float64)
+        Y = np.array(Y, dtype=np.float64, order="C").reshape(n, self.ns)
+        sol = None if solid is None else np.ascontiguousarray(solid, dtype=np.uint8)
+        nst = np.zeros(n, dtype=np.int64)
+        status = np.zeros(n, dtype=np.int32)
+        nth = nthreads or self.lib.or_max_threads()
+        self.lib.or_explicit_cells(self._sp, n, _ptr(rho), _ptr(e), _ptr(T), _ptr(Y), _ptr(sol), float(dt),
+                                   float(eps), float(T_min), int(kmax), int(nth), _ptr(nst), _ptr(status))
+        return dict(T=T, Y=Y, status=status, nsteps=nst)
 
     def max_threads(self):
         return self.lib.or_max_threads()

@@ -462,6 +462,65 @@ void or_integrate_cells(const omech* m, int64_t n, const double* rho, const doub
     }
 }
 
+/* The paper's explicit first-order adaptive scheme, written out
+ * step by step for algorithmic parity with the CUDA path's CHEM_METHOD_EXPLICIT:
+ *   Omega = rates(T, rho, Y); dY_k/dt = W_k Omega_k / rho                         (Eq. 5)
+ *   dt = min(eps * min_{k: Y_k > 1e-12, dY_k/dt != 0} Y_k / |dY_k/dt|, t_final - t),
+ *        the remaining time taken when the rule's step is within 1e-10 of it
+ *   Y <- max(Y + dt dY/dt, 0)  (clip, no renormalisation)
+ *   T <- Newton(e, Y) at constant (e, rho)
+ * while t < t_final and k < kmax.  status: 0 done, 1 gated, 2 unfinished (kmax), <0 failure. */
+void or_explicit_cells(const omech* m, int64_t n, const double* rho, const double* e, double* T, double* Y,
+                       const uint8_t* solid, double dt, double eps, double Tmin, int64_t kmax, int nthreads,
+                       int64_t* nsteps, int32_t* status)
+{
+    const int ns = m->ns;
+#pragma omp parallel for schedule(dynamic, 64) num_threads(nthreads)
+    for (int64_t i = 0; i < n; ++i) {
+        if (T[i] < Tmin || (solid && solid[i])) {
+            if (status) status[i] = 1;
+            if (nsteps) nsteps[i] = 0;
+            continue;
+        }
+        double* Yi = &Y[i * ns];
+        double Tc;
+        int rc = 0;
+        if (or_newton_T(m, e[i], Yi, T[i], &Tc) < 0) rc = -10;
+        double t = 0.0;
+        int64_t k = 0;
+        while (rc == 0 && t < dt && k < kmax) {
+            double w[OR_MAXS], f[OR_MAXS];
+            r_rates(m, rho[i], Tc, Yi, w, 0, 0);
+            double rmin = INFINITY;
+            for (int s = 0; s < ns; ++s) {
+                f[s] = m->W[s] * w[s] / rho[i];
+                if (Yi[s] > 1e-12 && f[s] != 0.0) {
+                    double r = Yi[s] / fabs(f[s]);
+                    if (r < rmin) rmin = r;
+                }
+            }
+            double h = eps * rmin;
+            /* land on t_final when the rule's step reaches it to 1e-10 relative (no sliver step
+             * from the rounding of t += h) */
+            int last = !(h < (dt - t) * (1.0 - 1e-10));
+            if (last) h = dt - t;
+            for (int s = 0; s < ns; ++s) {
+                double v = Yi[s] + h * f[s];
+                Yi[s] = v > 0.0 ? v : 0.0;
+            }
+            double Tn;
+            if (or_newton_T(m, e[i], Yi, Tc, &Tn) < 0) rc = -11;
+            Tc = Tn;
+            t = last ? dt : t + h;
+            ++k;
+        }
+        if (rc == 0 && t < dt) rc = 2;
+        T[i] = Tc;
+        if (status) status[i] = rc;
+        if (nsteps) nsteps[i] = k;
+    }
+}
+
 int or_max_threads(void)
 {
 #ifdef _OPENMP

@@ -18,6 +18,7 @@ LIB_PATH = pathlib.Path(__file__).resolve().parent / "libchem.so"
 
 CHEM_METHOD_RODAS4 = 0
 CHEM_METHOD_RODAS3 = 1
+CHEM_METHOD_EXPLICIT = 2
 
 _ERRORS = {-1: "CHEM_EINVAL", -2: "CHEM_EMECH", -3: "CHEM_ENOSTRUCT", -4: "CHEM_ECUDA", -5: "CHEM_ENOWS"}
 
@@ -41,7 +42,8 @@ class ChemMechDesc(ctypes.Structure):
 class ChemOpts(ctypes.Structure):
     _fields_ = [("T_min", ctypes.c_double), ("kmax_bulk", ctypes.c_int32), ("n_active_star", ctypes.c_int64),
                 ("kmax_sparse", ctypes.c_int32), ("atol_T", ctypes.c_double), ("method", ctypes.c_int32),
-                ("compact_bulk", ctypes.c_int32), ("lanes_per_cell", ctypes.c_int32)]
+                ("compact_bulk", ctypes.c_int32), ("lanes_per_cell", ctypes.c_int32),
+                ("eps_change", ctypes.c_double)]
 
 
 class ChemBox(ctypes.Structure):

@@ -194,7 +194,8 @@ struct MechOps {
                               int fin, int grid, cudaStream_t s)
     {
         auto kern = k_integrate<M, Meth, kIntegrateBS>;
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem<Meth>());
+        cudaError_t e = cudaSuccess;
+        if (smem<Meth>() > 0) e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem<Meth>());
         if (e != cudaSuccess) return e;
         kern<<<grid, kIntegrateBS, smem<Meth>(), s>>>(p, L, ids, n, kmax, refill, fin);
         return cudaGetLastError();
@@ -204,6 +205,7 @@ struct MechOps {
     {
         const P& p = *static_cast<const P*>(pp);
         if (method == CHEM_METHOD_RODAS3) return launch<Rodas3>(p, L, ids, n, kmax, refill, fin, grid, s);
+        if (method == CHEM_METHOD_EXPLICIT) return launch<Explicit>(p, L, ids, n, kmax, refill, fin, grid, s);
         return launch<Rodas4>(p, L, ids, n, kmax, refill, fin, grid, s);
     }
     template <class Meth>
@@ -211,11 +213,15 @@ struct MechOps {
     {
         int nb = 0;
         auto kern = k_integrate<M, Meth, kIntegrateBS>;
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem<Meth>());
+        if (smem<Meth>() > 0) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem<Meth>());
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kIntegrateBS, smem<Meth>());
         return std::max(nb, 1);
     }
-    static int blocks_per_sm(int method) { return method == CHEM_METHOD_RODAS3 ? bps<Rodas3>() : bps<Rodas4>(); }
+    static int blocks_per_sm(int method)
+    {
+        if (method == CHEM_METHOD_EXPLICIT) return bps<Explicit>();
+        return method == CHEM_METHOD_RODAS3 ? bps<Rodas3>() : bps<Rodas4>();
+    }
 
     // ---- lane-group kernel
     static constexpr int kGrpBS = MechOpsBS::kGrp;
@@ -425,6 +431,7 @@ void chem_default_opts(chem_opts* o)
     o->method = CHEM_METHOD_RODAS4;
     o->compact_bulk = 1;
     o->lanes_per_cell = 1;
+    o->eps_change = 0.01;
 }
 
 const char* chem_strerror(int code)
@@ -443,7 +450,8 @@ const char* chem_strerror(int code)
 static int check_opts(const chem_opts* o)
 {
     if (o->kmax_bulk < 1 || o->kmax_sparse < 1 || o->n_active_star < 0 || !(o->atol_T > 0.0) ||
-        (o->method != CHEM_METHOD_RODAS4 && o->method != CHEM_METHOD_RODAS3) || !std::isfinite(o->T_min) ||
+        (o->method != CHEM_METHOD_RODAS4 && o->method != CHEM_METHOD_RODAS3 && o->method != CHEM_METHOD_EXPLICIT) ||
+        !std::isfinite(o->T_min) || !(o->eps_change > 0.0 && o->eps_change <= 1.0) ||
         (o->lanes_per_cell != 1 && o->lanes_per_cell != 4 && o->lanes_per_cell != 8))
         return CHEM_EINVAL;
     return CHEM_OK;
@@ -626,6 +634,7 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
     L.atol = atol;
     L.atolT = o.atol_T;
     L.T_min = o.T_min;
+    L.eps_change = o.eps_change;
     uint32_t* ids0 = reinterpret_cast<uint32_t*>(base + W.ids0);
     uint32_t* idsA = reinterpret_cast<uint32_t*>(base + W.idsA);
     uint32_t* idsB = reinterpret_cast<uint32_t*>(base + W.idsB);
@@ -658,7 +667,7 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
         return r;
     };
 
-    const bool use_grp = o.lanes_per_cell > 1 && c->grp_ok;
+    const bool use_grp = o.lanes_per_cell > 1 && c->grp_ok && o.method != CHEM_METHOD_EXPLICIT;
 
     // ---- Alg. 3 §1: gate + count + index map
     CK(cudaEventRecord(c->ev[0], s));

@@ -51,6 +51,7 @@ struct LaunchCtx {
     int32_t* cell_steps;       // [total] attempted substeps summed over launches
     unsigned long long* stats; // [S_NSTATS]
     double rtol, atol, atolT, T_min;
+    double eps_change;          // explicit scheme: max fractional change per step
 };
 
 __device__ __forceinline__ int find_box(const LaunchCtx& L, int64_t g)
@@ -163,9 +164,10 @@ __global__ void __launch_bounds__(BS) k_box_cost(LaunchCtx L, const uint32_t* id
 template <class M, class Meth>
 struct SmemLayout {
     static constexpr int n = M::NSA + 1;
-    static constexpr int off_K = n * n;
-    static constexpr int off_piv = n * n + Meth::S * n;
-    static constexpr int doubles = off_piv + (n + 7) / 8;
+    static constexpr bool none = (Meth::S == 0);   // explicit scheme: no matrix, no stages
+    static constexpr int off_K = none ? 0 : n * n;
+    static constexpr int off_piv = none ? 0 : n * n + Meth::S * n;
+    static constexpr int doubles = none ? 0 : off_piv + (n + 7) / 8;
     static constexpr int bytes_per_thread = doubles * 8;
 };
 
@@ -329,6 +331,44 @@ __device__ __forceinline__ int ros_step(const Params<M>& P, const LaunchCtx& L, 
     return 0;
 }
 
+// One step of the paper's explicit scheme (struct Explicit).  The
+// integrated unknowns are Y; y[NSA] holds T = Newton(e, Y) after every step.  Returns 1, or -1 when
+// the step cannot proceed (non-finite rate or Newton failure).
+template <class M>
+__device__ __forceinline__ int explicit_step(const Params<M>& P, const LaunchCtx& L, Cell<M>& C, double eps,
+                                             Counters& cnt)
+{
+    constexpr int n = M::NSA + 1;
+    double f[n];
+    rhs<M>(P, C.rho, 1.0 / C.rho, C.y, C.Yin, f);
+    cnt.rhs++;
+    const double remaining = C.dt - C.t;
+    double rmin = INFINITY;
+#pragma unroll
+    for (int i = 0; i < M::NSA; ++i)
+        if (C.y[i] > Explicit::Y_floor && f[i] != 0.0) rmin = fmin(rmin, C.y[i] / fabs(f[i]));
+    double h = eps * rmin;
+    bool last = !(h < remaining * (1.0 - 1e-10));   // no sliver step from the rounding of t += h
+    if (last) h = remaining;
+    bool finite = true;
+#pragma unroll
+    for (int i = 0; i < M::NSA; ++i) {
+        C.y[i] = fmax(fma(h, f[i], C.y[i]), 0.0);   // clip to 0, no renormalisation
+        finite = finite && isfinite(C.y[i]);
+    }
+    double Yf[M::NS];
+    full_Y<M>(C.y, C.Yin, Yf);
+    double T = C.y[M::NSA];
+    const bool ok = newton_T<M>(P, C.e, Yf, T) && finite;
+    C.y[M::NSA] = T;
+    C.t = last ? C.dt : C.t + h;
+    C.k++;
+    cnt.attempted++;
+    cnt.accepted++;
+    if (!ok) { cnt.newton_fail++; return -1; }
+    return 1;
+}
+
 template <class M>
 __device__ __forceinline__ void load_cell(const Params<M>& P, const LaunchCtx& L, uint32_t g, Cell<M>& C,
                                           uint8_t st, Counters& cnt, bool& ok)
@@ -454,7 +494,9 @@ __global__ void __launch_bounds__(BS) k_integrate(const __grid_constant__ Params
             if (!ok) { L.state[g] = ST_FAILED; continue; }
             have = true;
         }
-        const int r = ros_step<M, Meth>(P, L, C, A, Ks, piv, BS, cnt);
+        int r;
+        if constexpr (Meth::S == 0) r = explicit_step<M>(P, L, C, L.eps_change, cnt);
+        else r = ros_step<M, Meth>(P, L, C, A, Ks, piv, BS, cnt);
         if (r < 0) {
             cnt.nonfinite++;
             store_cell<M>(P, L, C, ST_FAILED, cnt);

@@ -261,3 +261,26 @@ def test_boxes_fused_equals_single(chem, ora):
     c = cost.cpu().numpy()
     assert np.isclose(c.sum(), st["steps_attempted"])
     assert all(ci == s[2]["steps_attempted"] for ci, s in zip(c, singles))
+
+
+def test_explicit_paper_scheme_algorithmic_parity(ora):
+    """NEXT-1: the paper's explicit scheme on the CUDA path vs the oracle's step-by-step
+    implementation of the same rule: identical step counts, state within 1e-10 (algorithmic parity;
+    the two differ only in the rates' rounding: ln-space matrix form vs per-reaction products)."""
+    import synth as _s
+    doc = _s.load_trajectories()
+    d = _s.cfg1b(doc, n=512)
+    ch = Chem("h2air_li2004", device=0, method=2, eps_change=0.01, kmax_sparse=100000)
+    e = np.array([ora.energy(t, y) for t, y in zip(d["T"], d["Y"])])
+    out = ora.explicit_cells(d["rho"], e, d["T"], d["Y"], d["dt"], eps=0.01)
+    assert np.all(out["status"] == 0)
+    Td = to_dev(d["T"])
+    Yd = species_dev(d["Y"])
+    st = ch.integrate(to_dev(d["rho"]), to_dev(e), Td, Yd, d["dt"])
+    assert st["n_unfinished"] == 0 and st["n_nonfinite"] == 0
+    assert st["steps_attempted"] == int(out["nsteps"].sum())
+    assert out["nsteps"].max() >= 10            # many explicit steps per cell (P:172)
+    Tg, Yg = Td.cpu().numpy(), Yd.cpu().numpy().T
+    mask = out["Y"] > 1e-12
+    assert np.max(np.abs(Tg / out["T"] - 1)) < 1e-10
+    assert np.max(np.abs(Yg[mask] / out["Y"][mask] - 1)) < 1e-10
