@@ -41,7 +41,7 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--rtol", type=float, default=RTOL)
     p.add_argument("--atol", type=float, default=ATOL)
-    p.add_argument("--method", default="rodas4", choices=["rodas4", "rodas3", "explicit"])
+    p.add_argument("--method", default="rodas4", choices=["rodas4", "rodas3", "explicit", "ros4"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--cpu-sample-seconds", type=float, default=15.0)
@@ -319,12 +319,12 @@ def ours(args):
     device = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=device)
-    method = {"rodas4": 0, "rodas3": 1, "explicit": 2}[args.method]
+    method = {"rodas4": 0, "rodas3": 1, "explicit": 2, "ros4": 3}[args.method]
     chem = Chem("h2air_li2004", device=local, atol_T=ATOL_T, method=method, lanes_per_cell=args.lanes)
     doc = synth.load_trajectories()
     wl = build_workload(args, chem, doc, device, rank, world)
     ncells = sum(b.ncells for b in wl.boxes)
-    fm = FlopModel(chem.mech, stages={0: 6, 1: 4, 2: 0}[method])
+    fm = FlopModel(chem.mech, stages={0: 6, 1: 4, 2: 0, 3: 4}[method])
 
     for _ in range(args.warmup):
         wl.restore()

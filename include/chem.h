@@ -78,6 +78,7 @@ typedef struct {
 #define CHEM_METHOD_EXPLICIT 2 /* the paper's explicit 1st-order adaptive scheme: dt limited so
                                   no Y_k (> 1e-12) changes by more than eps_change of itself; Euler
                                   update clipped at 0; T from Newton every step    */
+#define CHEM_METHOD_ROS4 3     /* Shampine's ROS4: 4 stages / 3 RHS per step, order 4, embedded 3    */
 
 typedef struct {
     double T_min;           /* gate T_reaction_min (value unstated -> 500 K) */

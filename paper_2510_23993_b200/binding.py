@@ -19,6 +19,7 @@ LIB_PATH = pathlib.Path(__file__).resolve().parent / "libchem.so"
 CHEM_METHOD_RODAS4 = 0
 CHEM_METHOD_RODAS3 = 1
 CHEM_METHOD_EXPLICIT = 2
+CHEM_METHOD_ROS4 = 3
 
 _ERRORS = {-1: "CHEM_EINVAL", -2: "CHEM_EMECH", -3: "CHEM_ENOSTRUCT", -4: "CHEM_ECUDA", -5: "CHEM_ENOWS"}
 

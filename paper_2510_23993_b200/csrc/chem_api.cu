@@ -206,6 +206,7 @@ struct MechOps {
         const P& p = *static_cast<const P*>(pp);
         if (method == CHEM_METHOD_RODAS3) return launch<Rodas3>(p, L, ids, n, kmax, refill, fin, grid, s);
         if (method == CHEM_METHOD_EXPLICIT) return launch<Explicit>(p, L, ids, n, kmax, refill, fin, grid, s);
+        if (method == CHEM_METHOD_ROS4) return launch<Ros4>(p, L, ids, n, kmax, refill, fin, grid, s);
         return launch<Rodas4>(p, L, ids, n, kmax, refill, fin, grid, s);
     }
     template <class Meth>
@@ -220,6 +221,7 @@ struct MechOps {
     static int blocks_per_sm(int method)
     {
         if (method == CHEM_METHOD_EXPLICIT) return bps<Explicit>();
+        if (method == CHEM_METHOD_ROS4) return bps<Ros4>();
         return method == CHEM_METHOD_RODAS3 ? bps<Rodas3>() : bps<Rodas4>();
     }
 
@@ -450,7 +452,7 @@ const char* chem_strerror(int code)
 static int check_opts(const chem_opts* o)
 {
     if (o->kmax_bulk < 1 || o->kmax_sparse < 1 || o->n_active_star < 0 || !(o->atol_T > 0.0) ||
-        (o->method != CHEM_METHOD_RODAS4 && o->method != CHEM_METHOD_RODAS3 && o->method != CHEM_METHOD_EXPLICIT) ||
+        (o->method < CHEM_METHOD_RODAS4 || o->method > CHEM_METHOD_ROS4) ||
         !std::isfinite(o->T_min) || !(o->eps_change > 0.0 && o->eps_change <= 1.0) ||
         (o->lanes_per_cell != 1 && o->lanes_per_cell != 4 && o->lanes_per_cell != 8))
         return CHEM_EINVAL;
@@ -667,7 +669,8 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
         return r;
     };
 
-    const bool use_grp = o.lanes_per_cell > 1 && c->grp_ok && o.method != CHEM_METHOD_EXPLICIT;
+    const bool use_grp = o.lanes_per_cell > 1 && c->grp_ok &&
+                         (o.method == CHEM_METHOD_RODAS4 || o.method == CHEM_METHOD_RODAS3);
 
     // ---- Alg. 3 §1: gate + count + index map
     CK(cudaEventRecord(c->ev[0], s));

@@ -246,16 +246,21 @@ __device__ __forceinline__ int ros_step(const Params<M>& P, const LaunchCtx& L, 
     const bool ok = lu_factor<n>(A, piv, ss);
 
     const double hinv = 1.0 / h;
+    double Flast[Meth::reuse_last ? n : 1];   // f of the last new stage point (methods reusing it)
     {   // stage 0: K_0 = A^{-1} f(y)
         double x[n];
 #pragma unroll
         for (int i = 0; i < n; ++i) Ks[i * ss] = f0[i];
+        if constexpr (Meth::reuse_last) {
+#pragma unroll
+            for (int i = 0; i < n; ++i) Flast[i] = f0[i];
+        }
         lu_solve<n>(A, piv, ss, Ks, ss, x);
     }
 #pragma unroll 1
     for (int s = 1; s < S; ++s) {
         double F[n];
-        if (Meth::newf_rt(s)) {
+        if (!Meth::reuse_last || Meth::newf_rt(s)) {
             double ys[n];
 #pragma unroll
             for (int i = 0; i < n; ++i) ys[i] = C.y[i];
@@ -269,10 +274,14 @@ __device__ __forceinline__ int ros_step(const Params<M>& P, const LaunchCtx& L, 
             }
             rhs<M>(P, C.rho, invrho, ys, C.Yin, F);
             cnt.rhs++;
-        } else {
-            // a_sj = 0 for all j (RODAS3 stage 1): the stage argument is y itself, f = f(y)
+            if constexpr (Meth::reuse_last) {
 #pragma unroll
-            for (int i = 0; i < n; ++i) F[i] = f0[i];
+                for (int i = 0; i < n; ++i) Flast[i] = F[i];
+            }
+        } else {
+            // the stage point equals the previous new one (a_sj = a_(s-1)j): reuse its f
+#pragma unroll
+            for (int i = 0; i < n; ++i) F[i] = Flast[i];
         }
 #pragma unroll
         for (int j = 0; j < S - 1; ++j) {

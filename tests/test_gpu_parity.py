@@ -284,3 +284,19 @@ def test_explicit_paper_scheme_algorithmic_parity(ora):
     mask = out["Y"] > 1e-12
     assert np.max(np.abs(Tg / out["T"] - 1)) < 1e-10
     assert np.max(np.abs(Yg[mask] / out["Y"][mask] - 1)) < 1e-10
+
+
+@pytest.mark.parametrize("method", [1, 3], ids=["rodas3", "ros4"])
+@pytest.mark.parametrize("cfg", ["cfg1", "cfg1c"])
+def test_integrate_parity_other_rosenbrock(ora, cfg, method):
+    """RODAS3 and Shampine's ROS4 reach the same 1e-6 parity bar at the parity tolerance."""
+    ch = Chem("h2air_li2004", device=0, atol_T=1e-6, method=method)
+    m = ora.m
+    d = getattr(synth, cfg)(m.species, m.W)
+    idx = np.arange(0, 4096, 8) if cfg == "cfg1" else np.arange(0, 4096, 32)
+    rho, T0, Y = d["rho"][idx], d["T"][idx], d["Y"][idx]
+    e = np.array([ora.energy(t, y) for t, y in zip(T0, Y)])
+    out = ora.integrate_cells(rho, e, T0, Y, d["dt"], **ORA_TOL)
+    T, Yg, st = _run_gpu(ch, rho, e, T0, Y, d["dt"])
+    assert st["n_unfinished"] == 0 and st["n_nonfinite"] == 0
+    _check_state(T, Yg, out, (cfg, method))

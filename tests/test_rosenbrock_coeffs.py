@@ -43,15 +43,26 @@ def _conditions(A, C, m, gamma):
     ]), alpha
 
 
+def _e_vector(struct, s):
+    body = SRC[SRC.index(f"struct {struct} {{"):]
+    ebody = body[body.index("e(int i)"):][:400]
+    m = re.search(r"constexpr double t\[\d+\] = \{([^}]*)\};", ebody)
+    if m:
+        return np.array([eval(x) for x in m.group(1).split(",")], dtype=float)
+    e = np.zeros(s); e[-1] = 1.0          # "return i == S-1 ? 1 : 0"
+    return e
+
+
 @pytest.mark.parametrize("struct,Aname,Cname,gamma,order", [("Rodas4", "kRodas4A", "kRodas4C", 0.25, 4),
-                                                          ("Rodas3", "kRodas3A", "kRodas3C", 0.5, 3)])
+                                                          ("Rodas3", "kRodas3A", "kRodas3C", 0.5, 3),
+                                                          ("Ros4", "kRos4A", "kRos4C", 0.5, 4)])
 def test_order_conditions(struct, Aname, Cname, gamma, order):
     A, C, m = _table(Aname), _table(Cname), _m_vector(struct)
     res, alpha = _conditions(A, C, m, gamma)
     nconds = {3: 4, 4: 8}[order]
     assert np.max(np.abs(res[:nconds])) < 1e-13, res
     # embedded method (m - e, e = last stage) is one order lower
-    e = np.zeros(len(m)); e[-1] = 1.0
+    e = _e_vector(struct, len(m))
     res_e, _ = _conditions(A, C, m - e, gamma)
     nlow = {3: 2, 4: 4}[order]
     assert np.max(np.abs(res_e[:nlow])) < 1e-13
