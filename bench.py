@@ -47,6 +47,8 @@ def parse():
     p.add_argument("--cpu-sample-seconds", type=float, default=15.0)
     p.add_argument("--balance", default="lpt", choices=["lpt", "none"])
     p.add_argument("--lanes", type=int, default=1, choices=[1, 4, 8], help="lanes per cell (1: thread per cell)")
+    p.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                   help="process-group backend (gloo only to exercise N>1 on a box with fewer GPUs)")
     return p.parse_args()
 
 
@@ -315,10 +317,14 @@ def ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=device)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=device)
+        else:
+            dist.init_process_group("gloo")
     method = {"rodas4": 0, "rodas3": 1, "explicit": 2, "ros4": 3}[args.method]
     chem = Chem("h2air_li2004", device=local, atol_T=ATOL_T, method=method, lanes_per_cell=args.lanes)
     doc = synth.load_trajectories()
@@ -352,12 +358,9 @@ def ours(args):
     t_rank = t_total
     tot_cs = wl.cell_steps
     if world > 1:
-        t = torch.tensor([t_total], dtype=torch.float64, device=device)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_total = float(t.item())
-        c = torch.tensor([float(wl.cell_steps)], dtype=torch.float64, device=device)
-        dist.all_reduce(c, op=dist.ReduceOp.SUM)
-        tot_cs = float(c.item())
+        from paper_2510_23993_b200 import sharding
+        t_total = float(sharding.reduce_stats([t_total], "max")[0])          # max over ranks
+        tot_cs = float(sharding.reduce_stats([float(wl.cell_steps)], "sum")[0])
     value = tot_cs * args.steps / t_total / 1e6
 
     # roofline of the dominant kernel (k_integrate: bulk + sparse launches, CUDA-event timed by the
@@ -395,9 +398,8 @@ def ours(args):
         torch.cuda.synchronize()
         te = sum(a.elapsed_time(b) for a, b in e_ev) / 1e3
         if world > 1:
-            t = torch.tensor([te], dtype=torch.float64, device=device)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            te = float(t.item())
+            from paper_2510_23993_b200 import sharding
+            te = float(sharding.reduce_stats([te], "max")[0])
         e2e = {"value": tot_cs * args.steps / te / 1e6, "unit": "Mcell-steps/s",
                "h2d_bytes_per_step": hr.h2d_bytes, "d2h_bytes_per_step": hr.d2h_bytes}
 

@@ -300,3 +300,49 @@ def test_integrate_parity_other_rosenbrock(ora, cfg, method):
     T, Yg, st = _run_gpu(ch, rho, e, T0, Y, d["dt"])
     assert st["n_unfinished"] == 0 and st["n_nonfinite"] == 0
     _check_state(T, Yg, out, (cfg, method))
+
+
+def test_fault_injection_counts(ora):
+    """SPEC S:184 / SURVEY §5: per-cell problems are counts, not call errors.  A tiny K_max_sparse
+    leaves cells unfinished (state at the last accepted step); NaN inputs are counted and do not
+    disturb the other cells; T far outside the NASA ranges is extrapolated and counted."""
+    m = ora.m
+    d = synth.cfg1c(m.species, m.W)
+    idx = np.arange(0, 4096, 64)
+    rho, T0, Y = d["rho"][idx].copy(), d["T"][idx].copy(), d["Y"][idx].copy()
+    e = np.array([ora.energy(t, y) for t, y in zip(T0, Y)])
+    ch = Chem("h2air_li2004", device=0, kmax_bulk=2, n_active_star=10 ** 9, kmax_sparse=3)
+    T, Yg, st = _run_gpu(ch, rho, e, T0, Y, d["dt"])
+    assert st["n_unfinished"] > 0 and st["n_nonfinite"] == 0
+    assert np.all(np.isfinite(T)) and np.all(np.isfinite(Yg))
+    # NaN in one cell's Y: counted as a failure, neighbours bitwise equal to a clean run
+    ch2 = Chem("h2air_li2004", device=0)
+    Tc, Yc, _ = _run_gpu(ch2, rho, e, T0, Y, 1e-7)
+    Yb = Y.copy()
+    Yb[5, 3] = np.nan
+    Tn, Yn, st2 = _run_gpu(ch2, rho, e, T0, Yb, 1e-7)
+    assert st2["n_nonfinite"] + st2["n_newton_fail"] >= 1
+    keep = np.arange(len(rho)) != 5
+    assert np.array_equal(Tn[keep], Tc[keep]) and np.array_equal(Yn[keep], Yc[keep])
+    # very hot cell: beyond the 3500 K NASA range -> counted in n_T_range, still finite
+    Th = np.full(4, 3200.0)
+    Yh = np.tile(d["Y"][0], (4, 1))
+    rh = synth.rho_ideal(synth.P_ATM * 30, Th, Yh, m.W)
+    eh = np.array([ora.energy(t, y) for t, y in zip(Th, Yh)])
+    Tg, Yg2, st3 = _run_gpu(ch2, rh, eh, Th, Yh, 1e-5)
+    assert np.all(np.isfinite(Tg)) and st3["n_T_range"] >= 1 and st3["n_unfinished"] == 0
+
+
+def test_invalid_arguments_are_errors():
+    from paper_2510_23993_b200.binding import ChemError
+    ch = Chem("h2air_li2004", device=0)
+    z = torch.zeros(4, dtype=torch.float64, device=DEV)
+    Y = torch.zeros((9, 4), dtype=torch.float64, device=DEV)
+    with pytest.raises(ChemError):
+        ch.integrate(z, z, z.clone(), Y, dt=-1.0)
+    with pytest.raises(ChemError):
+        ch.integrate(z, z, z.clone(), Y, dt=1e-7, rtol=0.0)
+    with pytest.raises(ChemError):
+        ch.set_opts(kmax_bulk=0)
+    with pytest.raises(TypeError):
+        ch.integrate(z.cpu(), z, z.clone(), Y, 1e-7)
