@@ -92,10 +92,16 @@ typedef struct {
     int32_t lanes_per_cell; /* 1: one thread integrates one cell; 4 or 8: a lane group shares one
                                cell (same mathematics, cooperative RHS/LU/solves) */
     double eps_change;      /* CHEM_METHOD_EXPLICIT: max fractional change per step (0.01; P:96 1-5%) */
+    int32_t temperature_mode; /* 0: T is an unknown integrated with Eq. 6 (corrected); 1: the
+                               unknowns are Y only and T = T(e, Y) by Newton at every RHS
+                               evaluation, dT/dY folded into the Jacobian               */
+    int32_t refill_bulk;    /* 1: bulk bursts also run as a persistent lane-refill grid (a lane whose
+                               cell ends its burst early takes the next id); 0: one thread per id */
 } chem_opts;
 
 /* fills the paper's defaults: 500 K, 5, 1e4, 1e5, 1e-6 K, RODAS4, compact_bulk = 1, lanes_per_cell = 1,
-   eps_change = 0.01 */
+   eps_change = 0.01, temperature_mode = 0,
+   refill_bulk = 0 */
 void chem_default_opts(chem_opts* o);
 
 /* ---- one AMR box / grid (FAB analogue) for the fused multi-box call ----------------- */

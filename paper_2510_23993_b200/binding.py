@@ -44,7 +44,8 @@ class ChemOpts(ctypes.Structure):
     _fields_ = [("T_min", ctypes.c_double), ("kmax_bulk", ctypes.c_int32), ("n_active_star", ctypes.c_int64),
                 ("kmax_sparse", ctypes.c_int32), ("atol_T", ctypes.c_double), ("method", ctypes.c_int32),
                 ("compact_bulk", ctypes.c_int32), ("lanes_per_cell", ctypes.c_int32),
-                ("eps_change", ctypes.c_double)]
+                ("eps_change", ctypes.c_double), ("temperature_mode", ctypes.c_int32),
+                ("refill_bulk", ctypes.c_int32)]
 
 
 class ChemBox(ctypes.Structure):

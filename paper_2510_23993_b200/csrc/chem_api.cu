@@ -38,11 +38,11 @@ struct Ops {
     cudaError_t (*temperature)(const void*, int64_t, int64_t, const double*, const double*, double*,
                                unsigned long long*, cudaStream_t);
     cudaError_t (*energy)(const void*, int64_t, int64_t, const double*, const double*, double*, cudaStream_t);
-    cudaError_t (*integrate)(const void*, int method, const LaunchCtx&, const uint32_t*, int64_t, int, int, int,
-                             int grid, cudaStream_t);
+    cudaError_t (*integrate)(const void*, int method, int dae, const LaunchCtx&, const uint32_t*, int64_t, int, int,
+                             int, int grid, cudaStream_t);
     cudaError_t (*integrate_grp)(const void* gtab, int method, int lanes, const LaunchCtx&, const uint32_t*, int64_t,
                                  int, int, int, int grid, cudaStream_t);
-    int (*blocks_per_sm)(int method);
+    int (*blocks_per_sm)(int method, int dae);
     int (*grp_blocks_per_sm)(int method, int lanes);
     size_t gtab_size;
     void (*build_gtab)(const void* params, void* out);
@@ -186,43 +186,58 @@ struct MechOps {
         return cudaGetLastError();
     }
 
-    template <class Meth>
-    static constexpr size_t smem() { return (size_t)SmemLayout<M, Meth>::bytes_per_thread * kIntegrateBS; }
+    template <class Meth, bool DAE = false>
+    static constexpr size_t smem() { return (size_t)SmemLayout<M, Meth, DAE>::bytes_per_thread * kIntegrateBS; }
 
-    template <class Meth>
+    template <class Meth, bool DAE>
     static cudaError_t launch(const P& p, const LaunchCtx& L, const uint32_t* ids, int64_t n, int kmax, int refill,
                               int fin, int grid, cudaStream_t s)
     {
-        auto kern = k_integrate<M, Meth, kIntegrateBS>;
+        auto kern = k_integrate<M, Meth, kIntegrateBS, DAE>;
         cudaError_t e = cudaSuccess;
-        if (smem<Meth>() > 0) e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem<Meth>());
+        if (smem<Meth, DAE>() > 0)
+            e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem<Meth, DAE>());
         if (e != cudaSuccess) return e;
-        kern<<<grid, kIntegrateBS, smem<Meth>(), s>>>(p, L, ids, n, kmax, refill, fin);
+        kern<<<grid, kIntegrateBS, smem<Meth, DAE>(), s>>>(p, L, ids, n, kmax, refill, fin);
         return cudaGetLastError();
     }
-    static cudaError_t integrate(const void* pp, int method, const LaunchCtx& L, const uint32_t* ids, int64_t n,
-                                 int kmax, int refill, int fin, int grid, cudaStream_t s)
+    template <bool DAE>
+    static cudaError_t integrate_t(const P& p, int method, const LaunchCtx& L, const uint32_t* ids, int64_t n,
+                                   int kmax, int refill, int fin, int grid, cudaStream_t s)
+    {
+        if (method == CHEM_METHOD_RODAS3) return launch<Rodas3, DAE>(p, L, ids, n, kmax, refill, fin, grid, s);
+        if (method == CHEM_METHOD_EXPLICIT) return launch<Explicit, false>(p, L, ids, n, kmax, refill, fin, grid, s);
+        if (method == CHEM_METHOD_ROS4) return launch<Ros4, DAE>(p, L, ids, n, kmax, refill, fin, grid, s);
+        return launch<Rodas4, DAE>(p, L, ids, n, kmax, refill, fin, grid, s);
+    }
+    static cudaError_t integrate(const void* pp, int method, int dae, const LaunchCtx& L, const uint32_t* ids,
+                                 int64_t n, int kmax, int refill, int fin, int grid, cudaStream_t s)
     {
         const P& p = *static_cast<const P*>(pp);
-        if (method == CHEM_METHOD_RODAS3) return launch<Rodas3>(p, L, ids, n, kmax, refill, fin, grid, s);
-        if (method == CHEM_METHOD_EXPLICIT) return launch<Explicit>(p, L, ids, n, kmax, refill, fin, grid, s);
-        if (method == CHEM_METHOD_ROS4) return launch<Ros4>(p, L, ids, n, kmax, refill, fin, grid, s);
-        return launch<Rodas4>(p, L, ids, n, kmax, refill, fin, grid, s);
+        return dae ? integrate_t<true>(p, method, L, ids, n, kmax, refill, fin, grid, s)
+                   : integrate_t<false>(p, method, L, ids, n, kmax, refill, fin, grid, s);
     }
-    template <class Meth>
+    template <class Meth, bool DAE>
     static int bps()
     {
         int nb = 0;
-        auto kern = k_integrate<M, Meth, kIntegrateBS>;
-        if (smem<Meth>() > 0) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem<Meth>());
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kIntegrateBS, smem<Meth>());
+        auto kern = k_integrate<M, Meth, kIntegrateBS, DAE>;
+        if (smem<Meth, DAE>() > 0)
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem<Meth, DAE>());
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kIntegrateBS, smem<Meth, DAE>());
         return std::max(nb, 1);
     }
-    static int blocks_per_sm(int method)
+    static int blocks_per_sm(int method, int dae)
     {
-        if (method == CHEM_METHOD_EXPLICIT) return bps<Explicit>();
-        if (method == CHEM_METHOD_ROS4) return bps<Ros4>();
-        return method == CHEM_METHOD_RODAS3 ? bps<Rodas3>() : bps<Rodas4>();
+        if (method == CHEM_METHOD_EXPLICIT) return bps<Explicit, false>();
+        if (dae) {
+            if (method == CHEM_METHOD_RODAS3) return bps<Rodas3, true>();
+            if (method == CHEM_METHOD_ROS4) return bps<Ros4, true>();
+            return bps<Rodas4, true>();
+        }
+        if (method == CHEM_METHOD_RODAS3) return bps<Rodas3, false>();
+        if (method == CHEM_METHOD_ROS4) return bps<Ros4, false>();
+        return bps<Rodas4, false>();
     }
 
     // ---- lane-group kernel
@@ -288,7 +303,7 @@ struct MechOps {
         o.grp_blocks_per_sm = &grp_blocks_per_sm;
         o.gtab_size = sizeof(GTable<M>);
         o.build_gtab = &build_gtab;
-        o.integrate_smem = smem<Rodas4>();
+        o.integrate_smem = smem<Rodas4, false>();
         return o;
     }
 };
@@ -434,6 +449,8 @@ void chem_default_opts(chem_opts* o)
     o->compact_bulk = 1;
     o->lanes_per_cell = 1;
     o->eps_change = 0.01;
+    o->temperature_mode = 0;
+    o->refill_bulk = 0;
 }
 
 const char* chem_strerror(int code)
@@ -454,6 +471,7 @@ static int check_opts(const chem_opts* o)
     if (o->kmax_bulk < 1 || o->kmax_sparse < 1 || o->n_active_star < 0 || !(o->atol_T > 0.0) ||
         (o->method < CHEM_METHOD_RODAS4 || o->method > CHEM_METHOD_ROS4) ||
         !std::isfinite(o->T_min) || !(o->eps_change > 0.0 && o->eps_change <= 1.0) ||
+        (o->temperature_mode != 0 && o->temperature_mode != 1) || (o->refill_bulk != 0 && o->refill_bulk != 1) ||
         (o->lanes_per_cell != 1 && o->lanes_per_cell != 4 && o->lanes_per_cell != 8))
         return CHEM_EINVAL;
     return CHEM_OK;
@@ -669,7 +687,7 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
         return r;
     };
 
-    const bool use_grp = o.lanes_per_cell > 1 && c->grp_ok &&
+    const bool use_grp = o.lanes_per_cell > 1 && c->grp_ok && o.temperature_mode == 0 &&
                          (o.method == CHEM_METHOD_RODAS4 || o.method == CHEM_METHOD_RODAS3);
 
     // ---- Alg. 3 §1: gate + count + index map
@@ -694,8 +712,14 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
         if (use_grp)
             CK(ops.integrate_grp(c->d_gtab, o.method, o.lanes_per_cell, L, lst, nl, o.kmax_bulk, 0, 0,
                                  (int)((nl * o.lanes_per_cell + MechOpsBS::kGrp - 1) / MechOpsBS::kGrp), s));
-        else
-            CK(ops.integrate(c->params.data(), o.method, L, lst, nl, o.kmax_bulk, 0, 0,
+        else if (o.refill_bulk) {
+            // persistent grid; a lane whose cell finishes its burst early takes the next id
+            CK(cudaMemsetAsync(L.stats + S_CURSOR, 0, 8, s));
+            const int grid = std::max(1, std::min<int>(c->num_sms * ops.blocks_per_sm(o.method, o.temperature_mode),
+                                                       (int)((nl + kIntegrateBS - 1) / kIntegrateBS)));
+            CK(ops.integrate(c->params.data(), o.method, o.temperature_mode, L, lst, nl, o.kmax_bulk, 1, 0, grid, s));
+        } else
+            CK(ops.integrate(c->params.data(), o.method, o.temperature_mode, L, lst, nl, o.kmax_bulk, 0, 0,
                              (int)((nl + kIntegrateBS - 1) / kIntegrateBS), s));
         CK(cudaEventRecord(c->ev[1], s));
         CK(cudaEventSynchronize(c->ev[1]));
@@ -724,9 +748,10 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
                                                        (int)((n_cur + cells_per_block - 1) / cells_per_block)));
             CK(ops.integrate_grp(c->d_gtab, o.method, o.lanes_per_cell, L, cur, n_cur, o.kmax_sparse, 1, 1, grid, s));
         } else {
-            const int grid = std::max(1, std::min<int>(c->num_sms * ops.blocks_per_sm(o.method),
+            const int grid = std::max(1, std::min<int>(c->num_sms * ops.blocks_per_sm(o.method, o.temperature_mode),
                                                        (int)((n_cur + kIntegrateBS - 1) / kIntegrateBS)));
-            CK(ops.integrate(c->params.data(), o.method, L, cur, n_cur, o.kmax_sparse, 1, 1, grid, s));
+            CK(ops.integrate(c->params.data(), o.method, o.temperature_mode, L, cur, n_cur, o.kmax_sparse, 1, 1,
+                             grid, s));
         }
         CK(cudaEventRecord(c->ev[1], s));
     }

@@ -160,19 +160,20 @@ __global__ void __launch_bounds__(BS) k_box_cost(LaunchCtx L, const uint32_t* id
 // Per-thread shared memory: the n x n iteration matrix (I/(h gamma) - J, then its LU), an
 // n-vector scratch for the permuted right-hand side, and n pivot bytes.
 // Per-thread shared memory (stride = block size, conflict-free): the n x n iteration matrix
-// (I/(h gamma) - J, then its LU), the S stage vectors K_s, and n pivot bytes.
-template <class M, class Meth>
+// (I/(h gamma) - J, then its LU), the stored stage vectors K_s, and n pivot bytes.  n = NSA+1
+// (T integrated by Eq. 6) or NSA (DAE: T from Newton at every evaluation).  Stiffly accurate
+// methods (RODAS4) do not store the last stage: y_new = Y_last + K_last and err = K_last.
+template <class M, class Meth, bool DAE = false>
 struct SmemLayout {
-    static constexpr int n = M::NSA + 1;
+    static constexpr int n = DAE ? M::NSA : M::NSA + 1;
     static constexpr bool none = (Meth::S == 0);   // explicit scheme: no matrix, no stages
+    static constexpr int nK = Meth::stiff_last ? Meth::S - 1 : Meth::S;
     static constexpr int off_K = none ? 0 : n * n;
-    static constexpr int off_piv = none ? 0 : n * n + Meth::S * n;
+    static constexpr int off_piv = none ? 0 : n * n + nK * n;
     static constexpr int doubles = none ? 0 : off_piv + (n + 7) / 8;
     static constexpr int bytes_per_thread = doubles * 8;
 };
 
-// Per-thread event counters (32-bit: they stay in registers for the whole kernel; one Jacobian
-// and one LU per attempted step, so those two are derived from `attempted`).
 struct Counters {
     unsigned attempted = 0, accepted = 0, rhs = 0, newton_fail = 0, nonfinite = 0, trange = 0, unfinished = 0,
              done = 0, frozen = 0;
@@ -194,15 +195,25 @@ struct Cell {
 // One attempted Rosenbrock substep on cell C (A6).  Returns 1 accepted, 0 rejected, -1 failure.
 // The stage loop is a runtime loop (one inlined copy of the RHS in the kernel: the fully
 // unrolled version overflowed the instruction cache); stage vectors live in shared memory.
-template <class M, class Meth>
+// DAE: the unknowns are the reacting Y; C.y[NSA] carries T = T(e, Y) (Newton).
+template <class M, class Meth, bool DAE>
 __device__ __forceinline__ int ros_step(const Params<M>& P, const LaunchCtx& L, Cell<M>& C, const SMat& A,
                                         double* Ks, uint8_t* piv, int ss, Counters& cnt)
 {
-    constexpr int n = M::NSA + 1;
+    constexpr int n = DAE ? M::NSA : M::NSA + 1;
     constexpr int S = Meth::S;
     const double invrho = 1.0 / C.rho;
     double f0[n];
-    rhs_jac<M, false>(P, C.rho, C.y, C.Yin, f0, A);
+    if constexpr (DAE) {
+        double Yf[M::NS];
+        full_Y<M>(C.y, C.Yin, Yf);
+        double T = C.y[M::NSA];
+        if (!newton_T<M>(P, C.e, Yf, T)) return -1;
+        C.y[M::NSA] = T;
+        rhs_jac<M, JAC_DAE>(P, C.rho, C.y, C.Yin, f0, A);
+    } else {
+        rhs_jac<M, JAC_ODE>(P, C.rho, C.y, C.Yin, f0, A);
+    }
     cnt.rhs++;
     const double remaining = C.dt - C.t;
     if (!(C.h > 0.0)) {
@@ -247,6 +258,8 @@ __device__ __forceinline__ int ros_step(const Params<M>& P, const LaunchCtx& L, 
 
     const double hinv = 1.0 / h;
     double Flast[Meth::reuse_last ? n : 1];   // f of the last new stage point (methods reusing it)
+    double ylast[n];                          // stage point of the last stage (stiffly accurate)
+    double xlast[n];                          // K of the last stage (not stored when stiff_last)
     {   // stage 0: K_0 = A^{-1} f(y)
         double x[n];
 #pragma unroll
@@ -257,13 +270,14 @@ __device__ __forceinline__ int ros_step(const Params<M>& P, const LaunchCtx& L, 
         }
         lu_solve<n>(A, piv, ss, Ks, ss, x);
     }
+    bool stage_ok = true;
 #pragma unroll 1
     for (int s = 1; s < S; ++s) {
         double F[n];
-        if (!Meth::reuse_last || Meth::newf_rt(s)) {
-            double ys[n];
+        double ys[n];
 #pragma unroll
-            for (int i = 0; i < n; ++i) ys[i] = C.y[i];
+        for (int i = 0; i < n; ++i) ys[i] = C.y[i];
+        if (!Meth::reuse_last || Meth::newf_rt(s)) {
 #pragma unroll
             for (int j = 0; j < S - 1; ++j) {
                 if (j < s) {
@@ -272,7 +286,12 @@ __device__ __forceinline__ int ros_step(const Params<M>& P, const LaunchCtx& L, 
                     for (int i = 0; i < n; ++i) ys[i] = fma(a, Ks[(j * n + i) * ss], ys[i]);
                 }
             }
-            rhs<M>(P, C.rho, invrho, ys, C.Yin, F);
+            if constexpr (DAE) {
+                double Ts = C.y[M::NSA];
+                stage_ok = rhs_dae<M>(P, C.rho, invrho, C.e, ys, C.Yin, Ts, F) && stage_ok;
+            } else {
+                rhs<M>(P, C.rho, invrho, ys, C.Yin, F);
+            }
             cnt.rhs++;
             if constexpr (Meth::reuse_last) {
 #pragma unroll
@@ -291,24 +310,37 @@ __device__ __forceinline__ int ros_step(const Params<M>& P, const LaunchCtx& L, 
                 for (int i = 0; i < n; ++i) F[i] = fma(c, Ks[(j * n + i) * ss], F[i]);
             }
         }
-        double* v = Ks + (s * n) * ss;
+        // the last stage of a stiffly accurate method solves in slot 0 (K_0 is no longer needed)
+        const bool last_stage = Meth::stiff_last && (s == S - 1);
+        double* v = Ks + ((last_stage ? 0 : s) * n) * ss;
 #pragma unroll
         for (int i = 0; i < n; ++i) v[i * ss] = F[i];
         double x[n];
         lu_solve<n>(A, piv, ss, v, ss, x);
+        if (last_stage) {
+#pragma unroll
+            for (int i = 0; i < n; ++i) { ylast[i] = ys[i]; xlast[i] = x[i]; }
+        }
     }
 
     double ynew[n];
     double err = 0.0;
 #pragma unroll
     for (int i = 0; i < n; ++i) {
-        double v = C.y[i], ev = 0.0;
-        static_for<0, S>([&](auto j_) {
-            constexpr int j = decltype(j_)::value;
-            const double kj = Ks[(j * n + i) * ss];
-            if constexpr (Meth::m(j) != 0.0) v = fma(Meth::m(j), kj, v);
-            if constexpr (Meth::e(j) != 0.0) ev = fma(Meth::e(j), kj, ev);
-        });
+        double v, ev;
+        if constexpr (Meth::stiff_last) {
+            v = ylast[i] + xlast[i];      // y + sum m_j K_j = Y_last + K_last
+            ev = xlast[i];                // sum e_j K_j = K_last
+        } else {
+            v = C.y[i];
+            ev = 0.0;
+            static_for<0, S>([&](auto j_) {
+                constexpr int j = decltype(j_)::value;
+                const double kj = Ks[(j * n + i) * ss];
+                if constexpr (Meth::m(j) != 0.0) v = fma(Meth::m(j), kj, v);
+                if constexpr (Meth::e(j) != 0.0) ev = fma(Meth::e(j), kj, ev);
+            });
+        }
         ynew[i] = v;
         const double s = ((i < M::NSA) ? L.atol : L.atolT) + L.rtol * fmax(fabs(C.y[i]), fabs(v));
         err = fma(ev / s, ev / s, err);
@@ -316,7 +348,7 @@ __device__ __forceinline__ int ros_step(const Params<M>& P, const LaunchCtx& L, 
     err = sqrt(err / n);
     cnt.attempted++;
     C.k++;
-    if (!ok || !isfinite(err)) {  // singular matrix or non-finite stage: shrink hard, retry
+    if (!ok || !stage_ok || !isfinite(err)) {  // singular matrix or non-finite stage: shrink hard, retry
         C.h = h * 0.1;
         C.rej = true;
         return 0;
@@ -468,13 +500,13 @@ __device__ __forceinline__ void flush_counters(const LaunchCtx& L, Counters& c)
 // all-cells launch) and runs <= kmax attempted substeps.  Sparse (refill = true): persistent
 // grid; each lane pulls ids from the atomic cursor S_CURSOR until the list is exhausted.
 // Both modes run the same substep code, so results are bitwise independent of K_max and N*.
-template <class M, class Meth, int BS>
+template <class M, class Meth, int BS, bool DAE = false>
 __global__ void __launch_bounds__(BS) k_integrate(const __grid_constant__ Params<M> P, LaunchCtx L,
                                                   const uint32_t* __restrict__ ids, int64_t n_ids, int kmax,
                                                   int refill, int final_phase)
 {
     extern __shared__ double smem[];
-    using SL = SmemLayout<M, Meth>;
+    using SL = SmemLayout<M, Meth, DAE>;
     constexpr int n = SL::n;
     double* mine = smem + threadIdx.x;
     SMat A{mine, BS, n};
@@ -505,7 +537,7 @@ __global__ void __launch_bounds__(BS) k_integrate(const __grid_constant__ Params
         }
         int r;
         if constexpr (Meth::S == 0) r = explicit_step<M>(P, L, C, L.eps_change, cnt);
-        else r = ros_step<M, Meth>(P, L, C, A, Ks, piv, BS, cnt);
+        else r = ros_step<M, Meth, DAE>(P, L, C, A, Ks, piv, BS, cnt);
         if (r < 0) {
             cnt.nonfinite++;
             store_cell<M>(P, L, C, ST_FAILED, cnt);
@@ -574,7 +606,7 @@ __global__ void __launch_bounds__(BS) k_jacobian(const __grid_constant__ Params<
 #pragma unroll
     for (int k = 0; k < M::NS; ++k) { y[k] = Y[k * ld + i]; Yd[k] = y[k]; }
     y[M::NS] = T[i];
-    rhs_jac<M, true>(P, rho[i], y, Yd, f, A);
+    rhs_jac<M, JAC_FULL>(P, rho[i], y, Yd, f, A);
 #pragma unroll
     for (int r = 0; r < nn; ++r)
 #pragma unroll

@@ -166,3 +166,37 @@ def test_cfg5_rank_shard(chem, ora, doc):
             if len(pool):
                 picks.append((b, int(rng.choice(pool))))
     _sample_and_check(ora, raw, boxes, picks)
+
+
+def test_virtual_ranks_bitwise(chem, ora, doc):
+    """per-cell results do not depend on the box -> rank map.  One copy of the
+    cfg4 hierarchy integrated as one fused call equals the same boxes split over 'virtual ranks'
+    (LPT on their measured cost, each rank's boxes in its own fused call), bitwise."""
+    from paper_2510_23993_b200.sharding import lpt_partition
+    m = ora.m
+    descs = [d for d in synth.hierarchy_cfg4(copy=2) if d["index"] % 4 == 0]     # 48 boxes, 3 levels
+    raw = [synth.build_cfg4_box(doc, m.W, m.species, d, DEV) for d in descs]
+    whole, st, cost = _run(chem, raw)
+    owner = lpt_partition(cost.cpu().numpy(), 3)
+    for r in range(3):
+        mine = [i for i in range(len(raw)) if owner[i] == r]
+        if not mine:
+            continue
+        part, _, _ = _run(chem, [raw[i] for i in mine])
+        for j, i in enumerate(mine):
+            assert torch.equal(part[j].T, whole[i].T) and torch.equal(part[j].Y, whole[i].Y)
+
+
+@pytest.mark.parametrize("opts", [dict(refill_bulk=1), dict(kmax_bulk=20, n_active_star=3000),
+                                  dict(compact_bulk=0, kmax_bulk=3)])
+def test_cfg3_schedule_variants_bitwise(ora, doc, opts):
+    """Bulk-sparse variants (lane-refill bursts, longer bursts, the paper's all-cells bursts) give
+    bitwise the same field as the default schedule (P:177 / S:191), at full cfg3 size."""
+    m = ora.m
+    ids = [0, 16, 32, 48]                    # the four boxes along y at x = 0 (band + spots)
+    raw, _ = synth.field_cfg3(doc, m.W, m.species, device=DEV, box_ids=ids)
+    ref, st0, _ = _run(Chem("h2air_li2004", device=0, atol_T=1e-6), raw)
+    alt, st1, _ = _run(Chem("h2air_li2004", device=0, atol_T=1e-6, **opts), raw)
+    for a, b in zip(ref, alt):
+        assert torch.equal(a.T, b.T) and torch.equal(a.Y, b.Y)
+    assert st0["steps_attempted"] == st1["steps_attempted"]

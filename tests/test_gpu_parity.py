@@ -286,11 +286,13 @@ def test_explicit_paper_scheme_algorithmic_parity(ora):
     assert np.max(np.abs(Yg[mask] / out["Y"][mask] - 1)) < 1e-10
 
 
-@pytest.mark.parametrize("method", [1, 3], ids=["rodas3", "ros4"])
+@pytest.mark.parametrize("method,tmode", [(1, 0), (3, 0), (0, 1), (1, 1)],
+                         ids=["rodas3", "ros4", "rodas4-dae", "rodas3-dae"])
 @pytest.mark.parametrize("cfg", ["cfg1", "cfg1c"])
-def test_integrate_parity_other_rosenbrock(ora, cfg, method):
-    """RODAS3 and Shampine's ROS4 reach the same 1e-6 parity bar at the parity tolerance."""
-    ch = Chem("h2air_li2004", device=0, atol_T=1e-6, method=method)
+def test_integrate_parity_other_rosenbrock(ora, cfg, method, tmode):
+    """RODAS3, Shampine's ROS4, and the DAE temperature mode (T = Newton(e, Y) at every RHS
+    evaluation) reach the same 1e-6 parity bar at the parity tolerance."""
+    ch = Chem("h2air_li2004", device=0, atol_T=1e-6, method=method, temperature_mode=tmode)
     m = ora.m
     d = getattr(synth, cfg)(m.species, m.W)
     idx = np.arange(0, 4096, 8) if cfg == "cfg1" else np.arange(0, 4096, 32)

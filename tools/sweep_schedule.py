@@ -43,6 +43,8 @@ def main():
     ap.add_argument("configs", nargs="*", default=["cfg3", "cfg4"])
     ap.add_argument("--kmax", default="5,20,100")
     ap.add_argument("--nstar", default="1e4,3e4,1e5,3e5,1e9")
+    ap.add_argument("--refill", default="0")
+    ap.add_argument("--no-fusion", action="store_true")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     doc = synth.load_trajectories()
@@ -51,16 +53,20 @@ def main():
         a = argparse.Namespace(config=cfg, rtol=bench.RTOL, atol=bench.ATOL, balance="none")
         wl = bench.build_workload(a, chem, doc, dev, 0, 1)
         base = None
-        for km in [int(x) for x in args.kmax.split(",")]:
+        for rf in [int(x) for x in args.refill.split(",")]:
+          for km in [int(x) for x in args.kmax.split(",")]:
             for ns in [int(float(x)) for x in args.nstar.split(",")]:
-                chem.set_opts(kmax_bulk=km, n_active_star=ns, compact_bulk=1)
+                chem.set_opts(kmax_bulk=km, n_active_star=ns, compact_bulk=1, refill_bulk=rf)
                 ms, st = time_step(wl, chem)
                 base = base or ms
                 print(json.dumps(dict(exp="schedule", config=cfg, kmax_bulk=km, n_active_star=ns, compact_bulk=1,
+                                      refill_bulk=rf,
                                       ms_per_step=ms, bulk_iters=sum(s["bulk_iters"] for s in st),
                                       sparse_cells=sum(s["sparse_cells"] for s in st),
                                       Mcell_steps_per_s=wl.cell_steps / ms / 1e3)), flush=True)
-        chem.set_opts(kmax_bulk=5, n_active_star=10000, compact_bulk=0)   # the paper's Alg. 3 as written
+        if args.no_fusion:
+            continue
+        chem.set_opts(kmax_bulk=5, n_active_star=10000, compact_bulk=0, refill_bulk=0)   # Alg. 3 as written
         ms, st = time_step(wl, chem)
         print(json.dumps(dict(exp="schedule", config=cfg, kmax_bulk=5, n_active_star=10000, compact_bulk=0,
                               ms_per_step=ms, bulk_iters=sum(s["bulk_iters"] for s in st),
@@ -69,6 +75,8 @@ def main():
         chem.set_opts(kmax_bulk=5, n_active_star=10000, compact_bulk=1)
         del wl
         torch.cuda.empty_cache()
+    if args.no_fusion:
+        return
     # App. E fusion experiment: 1M cells of cfg2 state split into 1..512 boxes, one fused call vs a call per box
     raw, _ = synth.field_cfg2(doc, side=128, box=32, device=dev)
     st0 = raw[0]
