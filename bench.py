@@ -380,6 +380,13 @@ def ours(args):
         pass
     peak = fp64_peak_tflops(sm_mhz=sm_mhz_peak)
     gpu_launches = sum(1 + 2 * s["bulk_iters"] + (1 if s["sparse_cells"] > 0 else 0) for s in stats)
+    traffic, ncu_pipe = None, None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(args.config)
+        if tr:
+            traffic, ncu_pipe = tr["traffic_bytes_per_launch"], tr.get("ncu_fp64_pipe_pct")
+    except Exception:
+        pass
 
     # e2e through the public API with host buffers (H2D + calls + D2H inside the timed region)
     e2e = None
@@ -433,7 +440,8 @@ def ours(args):
                        "l2": "inputs >= 369 MB/GPU > 126 MB L2 (no flush needed)",
                        "parallelism": f"boxes over {world} rank(s)", **wl.extra},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": None,
+                         "frac": achieved / peak, "traffic": traffic, "traffic_unit": "bytes per launch (ncu)",
+                         "ncu_fp64_pipe_pct": ncu_pipe,
                          "kernel": "k_integrate (bulk+sparse)", "flops_per_step_model": fm.per_step(),
                          "peak_source": "148 SMs x 64 FP64 FMA/clk x 2 x sm_max_mhz (derived, DESIGN.md)"},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches, "clocks": clk,
