@@ -17,7 +17,7 @@ using namespace chem;
 
 namespace {
 
-constexpr int kIntegrateBS = 64;   // threads per block of k_integrate (per-thread smem ~0.7 KB)
+constexpr int kIntegrateBS = 32;   // threads per block of k_integrate: 1008 B smem/thread -> 7 blocks/SM
 constexpr int kStreamBS = 256;     // gate / compaction / box cost
 constexpr int kPointBS = 128;      // point kernels
 struct MechOpsBS { static constexpr int kGrp = 128; };   // threads per block of k_integrate_grp

@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(BS) k_box_cost(LaunchCtx L, const uint32_t* id
 // Per-thread shared memory: the n x n iteration matrix (I/(h gamma) - J, then its LU), an
 // n-vector scratch for the permuted right-hand side, and n pivot bytes.
 // Per-thread shared memory (stride = block size, conflict-free): the n x n iteration matrix
-// (I/(h gamma) - J, then its LU), the stored stage vectors K_s, and n pivot bytes.  n = NSA+1
+// (I/(h gamma) - J, then its LU) and the stored stage vectors K_s (pivot rows stay in registers).  n = NSA+1
 // (T integrated by Eq. 6) or NSA (DAE: T from Newton at every evaluation).  Stiffly accurate
 // methods (RODAS4) do not store the last stage: y_new = Y_last + K_last and err = K_last.
 template <class M, class Meth, bool DAE = false>
@@ -169,8 +169,7 @@ struct SmemLayout {
     static constexpr bool none = (Meth::S == 0);   // explicit scheme: no matrix, no stages
     static constexpr int nK = Meth::stiff_last ? Meth::S - 1 : Meth::S;
     static constexpr int off_K = none ? 0 : n * n;
-    static constexpr int off_piv = none ? 0 : n * n + nK * n;
-    static constexpr int doubles = none ? 0 : off_piv + (n + 7) / 8;
+    static constexpr int doubles = none ? 0 : n * n + nK * n;   // pivots are kept in registers
     static constexpr int bytes_per_thread = doubles * 8;
 };
 
@@ -198,7 +197,7 @@ struct Cell {
 // DAE: the unknowns are the reacting Y; C.y[NSA] carries T = T(e, Y) (Newton).
 template <class M, class Meth, bool DAE>
 __device__ __forceinline__ int ros_step(const Params<M>& P, const LaunchCtx& L, Cell<M>& C, const SMat& A,
-                                        double* Ks, uint8_t* piv, int ss, Counters& cnt)
+                                        double* Ks, int ss, Counters& cnt)
 {
     constexpr int n = DAE ? M::NSA : M::NSA + 1;
     constexpr int S = Meth::S;
@@ -254,7 +253,8 @@ __device__ __forceinline__ int ros_step(const Params<M>& P, const LaunchCtx& L, 
     for (int i = 0; i < n; ++i)
 #pragma unroll
         for (int j = 0; j < n; ++j) A(i, j) = (i == j) ? ghinv - A(i, j) : -A(i, j);
-    const bool ok = lu_factor<n>(A, piv, ss);
+    uint64_t piv[(n + 7) / 8];
+    const bool ok = lu_factor<n>(A, piv);
 
     const double hinv = 1.0 / h;
     double Flast[Meth::reuse_last ? n : 1];   // f of the last new stage point (methods reusing it)
@@ -268,7 +268,7 @@ __device__ __forceinline__ int ros_step(const Params<M>& P, const LaunchCtx& L, 
 #pragma unroll
             for (int i = 0; i < n; ++i) Flast[i] = f0[i];
         }
-        lu_solve<n>(A, piv, ss, Ks, ss, x);
+        lu_solve<n>(A, piv, Ks, ss, x);
     }
     bool stage_ok = true;
 #pragma unroll 1
@@ -316,7 +316,7 @@ __device__ __forceinline__ int ros_step(const Params<M>& P, const LaunchCtx& L, 
 #pragma unroll
         for (int i = 0; i < n; ++i) v[i * ss] = F[i];
         double x[n];
-        lu_solve<n>(A, piv, ss, v, ss, x);
+        lu_solve<n>(A, piv, v, ss, x);
         if (last_stage) {
 #pragma unroll
             for (int i = 0; i < n; ++i) { ylast[i] = ys[i]; xlast[i] = x[i]; }
@@ -511,7 +511,6 @@ __global__ void __launch_bounds__(BS) k_integrate(const __grid_constant__ Params
     double* mine = smem + threadIdx.x;
     SMat A{mine, BS, n};
     double* Ks = mine + SL::off_K * BS;
-    uint8_t* piv = reinterpret_cast<uint8_t*>(smem + SL::off_piv * BS) + threadIdx.x;
 
     Counters cnt;
     Cell<M> C;
@@ -537,7 +536,7 @@ __global__ void __launch_bounds__(BS) k_integrate(const __grid_constant__ Params
         }
         int r;
         if constexpr (Meth::S == 0) r = explicit_step<M>(P, L, C, L.eps_change, cnt);
-        else r = ros_step<M, Meth, DAE>(P, L, C, A, Ks, piv, BS, cnt);
+        else r = ros_step<M, Meth, DAE>(P, L, C, A, Ks, BS, cnt);
         if (r < 0) {
             cnt.nonfinite++;
             store_cell<M>(P, L, C, ST_FAILED, cnt);
