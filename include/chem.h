@@ -171,6 +171,13 @@ int chem_integrate_boxes(chem_ctx* ctx, int32_t nboxes, const chem_box* boxes, d
                          double atol, void* ws, size_t ws_bytes, double* box_cost,
                          chem_stats* stats, void* stream);
 
+/* Activity trace (App. B: "the number of active cells after each integration step
+ * for every grid").  trace: DEVICE int32 [rows][nboxes] owned by the caller; subsequent
+ * chem_integrate* calls on this ctx write row 0 = active cells per box after the gate and row i =
+ * active cells per box after bulk launch i (i < rows; each launch is K_max attempted substeps per
+ * cell).  rows = 0 (or trace = NULL with rows = 0) turns tracing off. */
+int chem_set_trace(chem_ctx* ctx, int32_t* trace, int32_t rows);
+
 /* Test hooks and caller-side helpers ------------------------------------------------------ */
 /* T = Newton(e, Y) seeded with the incoming T.  T in/out [n]. */
 int chem_temperature(chem_ctx* ctx, int64_t n, int64_t ld, const double* e, const double* Y,

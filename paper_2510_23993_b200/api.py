@@ -85,6 +85,17 @@ class Chem:
         if rc != 0:
             raise _b.ChemError(rc, self.lib)
 
+    def set_trace(self, rows, nboxes):
+        """Enable the App. B activity trace: returns the device int32 [rows, nboxes] tensor that the
+        next integrate calls fill (row 0 after the gate, row i after bulk launch i)."""
+        if rows <= 0:
+            self._trace = None
+            self._call(self.lib.chem_set_trace(self._h, None, 0))
+            return None
+        self._trace = torch.zeros((rows, nboxes), dtype=torch.int32, device=self.device)
+        self._call(self.lib.chem_set_trace(self._h, _ptr(self._trace), rows))
+        return self._trace
+
     def _stream(self):
         return ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
 
@@ -210,3 +221,17 @@ class HostRunner:
             oT.copy_(d.T, non_blocking=True)
             oY.copy_(d.Y, non_blocking=True)
         return st
+
+
+def activity_lines(trace, boxes, levels=None, t=0.0, kmax=5):
+    """Format an activity trace in the paper's App. B line format:
+    'Level <level>, FAB <fab_ID>, t = <time>, step = <iteration>, n_cells = <total>, n_active = <active>'
+    (step = attempted-substep budget consumed: K_max per bulk launch)."""
+    tr = trace.cpu().numpy()
+    out = []
+    for b, bx in enumerate(boxes):
+        lv = 0 if levels is None else levels[b]
+        for it in range(tr.shape[0]):
+            out.append(f"Level {lv}, FAB {b}, t = {t:g}, step = {it * kmax}, n_cells = {bx.ncells}, "
+                       f"n_active = {int(tr[it, b])}")
+    return out

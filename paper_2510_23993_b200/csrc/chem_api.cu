@@ -400,6 +400,8 @@ struct chem_ctx {
     cudaEvent_t ev[2] = {nullptr, nullptr};
     void* d_gtab = nullptr;          // device copy of the lane-group kernel's table
     bool grp_ok = false;             // the group kernel needs one shared NASA T_mid
+    int32_t* trace = nullptr;        // device [trace_rows][nboxes] activity trace (App. B), or null
+    int32_t trace_rows = 0;
 };
 
 namespace {
@@ -535,6 +537,14 @@ void chem_finalize(chem_ctx* c)
 }
 
 const char* chem_structure_name(const chem_ctx* c) { return (c && c->ops) ? c->ops->name : ""; }
+
+int chem_set_trace(chem_ctx* c, int32_t* trace, int32_t rows)
+{
+    if (!c || rows < 0 || (rows > 0 && !trace)) return CHEM_EINVAL;
+    c->trace = rows > 0 ? trace : nullptr;
+    c->trace_rows = rows;
+    return CHEM_OK;
+}
 
 int chem_set_opts(chem_ctx* c, const chem_opts* o)
 {
@@ -699,6 +709,14 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
     CK(read_count(n_active));
     st.t_gate_ms = elapsed(c);
     st.active0 = n_active;
+    const bool tracing = c->trace && c->trace_rows > 0;
+    if (tracing) {
+        CK(cudaMemsetAsync(c->trace, 0, sizeof(int32_t) * (size_t)c->trace_rows * nboxes, s));
+        if (n_active > 0) {
+            k_box_count<kStreamBS><<<grid_for(n_active, kStreamBS), kStreamBS, 0, s>>>(L, ids0, n_active, c->trace);
+            CK(cudaGetLastError());
+        }
+    }
 
     // ---- Alg. 3 §2: bulk bursts while N_active > N*
     const uint32_t* cur = ids0;
@@ -733,6 +751,11 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
         st.t_compact_ms += elapsed(c);
         if (st.bulk_iters < 16) st.active_per_iter[st.bulk_iters] = n_cur;
         st.bulk_iters++;
+        if (tracing && st.bulk_iters < c->trace_rows && n_cur > 0) {
+            k_box_count<kStreamBS><<<grid_for(n_cur, kStreamBS), kStreamBS, 0, s>>>(
+                L, nxt, n_cur, c->trace + (size_t)st.bulk_iters * nboxes);
+            CK(cudaGetLastError());
+        }
         cur = nxt;
         nxt = (nxt == idsA) ? idsB : idsA;
     }

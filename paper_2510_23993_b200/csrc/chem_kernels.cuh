@@ -156,6 +156,24 @@ __global__ void __launch_bounds__(BS) k_box_cost(LaunchCtx L, const uint32_t* id
     }
 }
 
+// Activity trace (App. B): active cells of the index map per box.
+template <int BS>
+__global__ void __launch_bounds__(BS) k_box_count(LaunchCtx L, const uint32_t* ids, int64_t n, int32_t* row)
+{
+    for (int64_t base = (int64_t)blockIdx.x * BS; base < n; base += (int64_t)gridDim.x * BS) {
+        const int64_t i = base + threadIdx.x;
+        const bool valid = i < n;
+        const int b = valid ? find_box(L, ids[i]) : -1;
+        const int b0 = __shfl_sync(0xffffffffu, b, 0);
+        if (__all_sync(0xffffffffu, !valid || b == b0)) {
+            const int c = __popc(__ballot_sync(0xffffffffu, valid));
+            if ((threadIdx.x & 31) == 0 && b0 >= 0) atomicAdd(&row[b0], c);
+        } else if (valid) {
+            atomicAdd(&row[b], 1);
+        }
+    }
+}
+
 // ----------------------------------------------------------------------------- A6/A7/A9 integrate
 // Per-thread shared memory: the n x n iteration matrix (I/(h gamma) - J, then its LU), an
 // n-vector scratch for the permuted right-hand side, and n pivot bytes.

@@ -200,3 +200,23 @@ def test_cfg3_schedule_variants_bitwise(ora, doc, opts):
     for a, b in zip(ref, alt):
         assert torch.equal(a.T, b.T) and torch.equal(a.Y, b.Y)
     assert st0["steps_attempted"] == st1["steps_attempted"]
+
+
+def test_activity_trace_app_b(ora, doc):
+    """App. B instrumentation: per-box active counts after the gate and each bulk launch,
+    consistent with the gate count and the per-iteration totals; App. B line format."""
+    from paper_2510_23993_b200.api import activity_lines
+    m = ora.m
+    raw, _ = synth.field_cfg3(doc, m.W, m.species, device=DEV, box_ids=[0, 1, 16, 17])
+    ch = Chem("h2air_li2004", device=0, atol_T=1e-6, n_active_star=100)
+    tr = ch.set_trace(12, len(raw))
+    boxes, st, _ = _run(ch, raw)
+    t = tr.cpu().numpy()
+    for b, r in enumerate(raw):
+        assert t[0, b] == int((r["T"] >= 500).sum())
+    for i in range(1, min(12, st["bulk_iters"] + 1)):
+        assert t[i].sum() == st["active_per_iter"][i - 1]
+        assert np.all(t[i] <= t[i - 1])
+    lines = activity_lines(tr, boxes, t=1e-7, kmax=5)
+    assert lines[0].startswith("Level 0, FAB 0, t = 1e-07, step = 0, n_cells = 262144, n_active = ")
+    ch.set_trace(0, 0)
