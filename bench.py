@@ -49,6 +49,7 @@ def parse():
     p.add_argument("--lanes", type=int, default=1, choices=[1, 4, 8], help="lanes per cell (1: thread per cell)")
     p.add_argument("--tmode", type=int, default=0, choices=[0, 1],
                    help="0: T integrated by Eq. 6; 1: T = Newton(e, Y) at every RHS evaluation (P:96)")
+    p.add_argument("--h0", type=float, default=0.01, help="initial substep factor (chem_opts.h0_factor)")
     p.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                    help="process-group backend (gloo only to exercise N>1 on a box with fewer GPUs)")
     return p.parse_args()
@@ -329,7 +330,7 @@ def ours(args):
             dist.init_process_group("gloo")
     method = {"rodas4": 0, "rodas3": 1, "explicit": 2, "ros4": 3}[args.method]
     chem = Chem("h2air_li2004", device=local, atol_T=ATOL_T, method=method, lanes_per_cell=args.lanes,
-                temperature_mode=args.tmode)
+                temperature_mode=args.tmode, h0_factor=args.h0)
     doc = synth.load_trajectories()
     wl = build_workload(args, chem, doc, device, rank, world)
     ncells = sum(b.ncells for b in wl.boxes)
@@ -436,7 +437,7 @@ def ours(args):
             "config": {"workload": wl.meta["workload"], "cells_per_gpu": ncells, "boxes_per_gpu": len(wl.boxes),
                        "cell_steps_per_step_per_gpu": wl.cell_steps, "fused_calls_per_step": len(wl.calls),
                        "rtol": args.rtol, "atol_Y": args.atol, "atol_T": ATOL_T, "method": args.method,
-                       "lanes_per_cell": args.lanes, "temperature_mode": args.tmode,
+                       "lanes_per_cell": args.lanes, "temperature_mode": args.tmode, "h0_factor": args.h0,
                        "l2": "inputs >= 369 MB/GPU > 126 MB L2 (no flush needed)",
                        "parallelism": f"boxes over {world} rank(s)", **wl.extra},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",

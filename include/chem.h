@@ -97,11 +97,13 @@ typedef struct {
                                evaluation, dT/dY folded into the Jacobian               */
     int32_t refill_bulk;    /* 1: bulk bursts also run as a persistent lane-refill grid (a lane whose
                                cell ends its burst early takes the next id); 0: one thread per id */
+    double h0_factor;       /* first substep of a cell = h0_factor * |y|/|f(y)| (WRMS norms), capped
+                               at dt (Hairer-Norsett-Wanner I.II.4 use 0.01)                      */
 } chem_opts;
 
 /* fills the paper's defaults: 500 K, 5, 1e4, 1e5, 1e-6 K, RODAS4, compact_bulk = 1, lanes_per_cell = 1,
    eps_change = 0.01, temperature_mode = 0,
-   refill_bulk = 0 */
+   refill_bulk = 0, h0_factor = 0.01 */
 void chem_default_opts(chem_opts* o);
 
 /* ---- one AMR box / grid (FAB analogue) for the fused multi-box call ----------------- */

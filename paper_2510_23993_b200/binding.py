@@ -45,7 +45,7 @@ class ChemOpts(ctypes.Structure):
                 ("kmax_sparse", ctypes.c_int32), ("atol_T", ctypes.c_double), ("method", ctypes.c_int32),
                 ("compact_bulk", ctypes.c_int32), ("lanes_per_cell", ctypes.c_int32),
                 ("eps_change", ctypes.c_double), ("temperature_mode", ctypes.c_int32),
-                ("refill_bulk", ctypes.c_int32)]
+                ("refill_bulk", ctypes.c_int32), ("h0_factor", ctypes.c_double)]
 
 
 class ChemBox(ctypes.Structure):

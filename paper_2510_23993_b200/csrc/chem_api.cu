@@ -453,6 +453,7 @@ void chem_default_opts(chem_opts* o)
     o->eps_change = 0.01;
     o->temperature_mode = 0;
     o->refill_bulk = 0;
+    o->h0_factor = 0.01;
 }
 
 const char* chem_strerror(int code)
@@ -474,6 +475,7 @@ static int check_opts(const chem_opts* o)
         (o->method < CHEM_METHOD_RODAS4 || o->method > CHEM_METHOD_ROS4) ||
         !std::isfinite(o->T_min) || !(o->eps_change > 0.0 && o->eps_change <= 1.0) ||
         (o->temperature_mode != 0 && o->temperature_mode != 1) || (o->refill_bulk != 0 && o->refill_bulk != 1) ||
+        !(o->h0_factor > 0.0 && o->h0_factor <= 1.0) ||
         (o->lanes_per_cell != 1 && o->lanes_per_cell != 4 && o->lanes_per_cell != 8))
         return CHEM_EINVAL;
     return CHEM_OK;
@@ -665,6 +667,7 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
     L.atolT = o.atol_T;
     L.T_min = o.T_min;
     L.eps_change = o.eps_change;
+    L.h0_factor = o.h0_factor;
     uint32_t* ids0 = reinterpret_cast<uint32_t*>(base + W.ids0);
     uint32_t* idsA = reinterpret_cast<uint32_t*>(base + W.idsA);
     uint32_t* idsB = reinterpret_cast<uint32_t*>(base + W.idsB);

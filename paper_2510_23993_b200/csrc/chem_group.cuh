@@ -589,7 +589,7 @@ __device__ __forceinline__ int g_step(const GTable<M>& tb, const Grp<G>& gr, con
             cnt.frozen++;
             return 1;
         }
-        C.h = (d0 < 1e-5) ? remaining : fmin(remaining, 0.01 * d0 / d1);
+        C.h = (d0 < 1e-5) ? remaining : fmin(remaining, L.h0_factor * d0 / d1);
     }
     bool last = false;
     double h = C.h;

@@ -52,6 +52,7 @@ struct LaunchCtx {
     unsigned long long* stats; // [S_NSTATS]
     double rtol, atol, atolT, T_min;
     double eps_change;          // explicit scheme: max fractional change per step
+    double h0_factor;           // initial substep = h0_factor |y|/|f| (Hairer-Norsett-Wanner: 0.01)
 };
 
 __device__ __forceinline__ int find_box(const LaunchCtx& L, int64_t g)
@@ -258,7 +259,7 @@ __device__ __forceinline__ int ros_step(const Params<M>& P, const LaunchCtx& L, 
             cnt.frozen++;
             return 1;
         }
-        C.h = (d0 < 1e-5) ? remaining : fmin(remaining, 0.01 * d0 / d1);
+        C.h = (d0 < 1e-5) ? remaining : fmin(remaining, L.h0_factor * d0 / d1);
     }
     bool last = false;
     double h = C.h;
