@@ -49,6 +49,7 @@ def parse():
     p.add_argument("--lanes", type=int, default=1, choices=[1, 4, 8], help="lanes per cell (1: thread per cell)")
     p.add_argument("--tmode", type=int, default=0, choices=[0, 1],
                    help="0: T integrated by Eq. 6; 1: T = Newton(e, Y) at every RHS evaluation (P:96)")
+    p.add_argument("--e2e-chunks", type=int, default=0, help="e2e copy/compute pipelining groups (0: auto)")
     p.add_argument("--h0", type=float, default=0.01, help="initial substep factor (chem_opts.h0_factor)")
     p.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                    help="process-group backend (gloo only to exercise N>1 on a box with fewer GPUs)")
@@ -394,7 +395,10 @@ def ours(args):
     if not args.no_e2e:
         host = [dict(rho=b.rho.cpu().pin_memory(), e=b.e.cpu().pin_memory(), T=p[0].cpu().pin_memory(),
                      Y=p[1].cpu().pin_memory(), dt=b.dt) for b, p in zip(wl.boxes, wl.pristine)]
-        hr = HostRunner(chem, host, wl.calls)
+        # copy/compute pipelining pays on dense fields; on sparse ones (cfg3/cfg4) splitting the fused
+        # call serialises the chunks' long tails, so those run as one call
+        chunks = args.e2e_chunks if args.e2e_chunks > 0 else (4 if args.config in ("cfg2", "cfg5") else 1)
+        hr = HostRunner(chem, host, wl.calls, chunks=chunks)
         hr.step(args.rtol, args.atol)
         torch.cuda.synchronize()
         e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -412,7 +416,8 @@ def ours(args):
             from paper_2510_23993_b200 import sharding
             te = float(sharding.reduce_stats([te], "max")[0])
         e2e = {"value": tot_cs * args.steps / te / 1e6, "unit": "Mcell-steps/s",
-               "h2d_bytes_per_step": hr.h2d_bytes, "d2h_bytes_per_step": hr.d2h_bytes}
+               "h2d_bytes_per_step": hr.h2d_bytes, "d2h_bytes_per_step": hr.d2h_bytes,
+               "copy_compute_chunks": chunks if hr.pipelined else 1}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
