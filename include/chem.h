@@ -184,6 +184,9 @@ int chem_set_trace(chem_ctx* ctx, int32_t* trace, int32_t rows);
 /* T = Newton(e, Y) seeded with the incoming T.  T in/out [n]. */
 int chem_temperature(chem_ctx* ctx, int64_t n, int64_t ld, const double* e, const double* Y,
                      double* T, void* stream);
+/* PAPER.md Alg. 1, the caller-side step before chemistry: e = rho E/rho - |u|^2/2 from the
+ * conserved variables U[c*ld + i], c = 0..4 = rho, rho u_x, rho u_y, rho u_z, rho E (DEVICE). */
+int chem_internal_energy(chem_ctx* ctx, int64_t n, int64_t ld, const double* U, double* e, void* stream);
 /* e = u(T, Y) = sum_k Y_k eps_k(T)/W_k (the inverse of chem_temperature). */
 int chem_energy(chem_ctx* ctx, int64_t n, int64_t ld, const double* T, const double* Y, double* e,
                 void* stream);

@@ -142,6 +142,23 @@ class Chem:
         self._call(self.lib.chem_temperature(self._h, n, ld, _ptr(e), _ptr(Y), _ptr(T), self._stream()))
         return T
 
+    def internal_energy(self, U, out=None):
+        """Alg. 1: e = rho E/rho - |u|^2/2 from conserved U [5, ld] (component-major)."""
+        _check(U, "U")
+        if U.dim() != 2 or U.shape[0] != 5 or U.stride(1) != 1:
+            raise ValueError("U must be [5, ld]: rho, rho ux, rho uy, rho uz, rho E")
+        n = U.shape[1]
+        if out is None:
+            out = torch.empty(n, dtype=torch.float64, device=self.device)
+        self._call(self.lib.chem_internal_energy(self._h, n, U.stride(0), _ptr(U), _ptr(out), self._stream()))
+        return out
+
+    def strang_half_step(self, boxes, dt_flow, rtol=1e-9, atol=1e-20, box_cost=None):
+        """Chemistry half of a Strang-split flow step: integrate every box over dt_flow/2.
+        A flow solver calls this before and after its own dt_flow update."""
+        half = [Box(b.rho, b.e, b.T, b.Y, 0.5 * dt_flow, b.solid) for b in boxes]
+        return self.integrate_boxes(half, rtol=rtol, atol=atol, box_cost=box_cost)
+
     def energy(self, T, Y, out=None):
         n = T.shape[0]
         ld = _species(Y, self.ns)

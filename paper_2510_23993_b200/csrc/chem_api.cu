@@ -599,6 +599,15 @@ int chem_temperature(chem_ctx* c, int64_t n, int64_t ld, const double* e, const 
     return cuda_fail(c, c->ops->temperature(c->params.data(), n, ld, e, Y, T, nullptr, (cudaStream_t)stream));
 }
 
+int chem_internal_energy(chem_ctx* c, int64_t n, int64_t ld, const double* U, double* e, void* stream)
+{
+    CHEM_PRE(c);
+    if (n < 0 || ld < n || (n > 0 && (!U || !e))) return CHEM_EINVAL;
+    if (n == 0) return CHEM_OK;
+    k_internal_energy<<<grid_for(n, kPointBS), kPointBS, 0, (cudaStream_t)stream>>>(n, ld, U, e);
+    return cuda_fail(c, cudaGetLastError());
+}
+
 int chem_energy(chem_ctx* c, int64_t n, int64_t ld, const double* T, const double* Y, double* e, void* stream)
 {
     CHEM_PRE(c);
