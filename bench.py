@@ -51,6 +51,8 @@ def parse():
                    help="0: T integrated by Eq. 6; 1: T = Newton(e, Y) at every RHS evaluation (P:96)")
     p.add_argument("--e2e-chunks", type=int, default=0, help="e2e copy/compute pipelining groups (0: auto)")
     p.add_argument("--h0", type=float, default=0.01, help="initial substep factor (chem_opts.h0_factor)")
+    p.add_argument("--opt", action="append", default=[], metavar="KEY=VAL",
+                   help="extra chem_opts field (e.g. kmax_bulk=5, refill_bulk=1); repeatable")
     p.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                    help="process-group backend (gloo only to exercise N>1 on a box with fewer GPUs)")
     return p.parse_args()
@@ -331,7 +333,8 @@ def ours(args):
             dist.init_process_group("gloo")
     method = {"rodas4": 0, "rodas3": 1, "explicit": 2, "ros4": 3}[args.method]
     chem = Chem("h2air_li2004", device=local, atol_T=ATOL_T, method=method, lanes_per_cell=args.lanes,
-                temperature_mode=args.tmode, h0_factor=args.h0)
+                temperature_mode=args.tmode, h0_factor=args.h0,
+                **{k: float(v) if "." in v or "e" in v else int(v) for k, v in (o.split("=", 1) for o in args.opt)})
     doc = synth.load_trajectories()
     wl = build_workload(args, chem, doc, device, rank, world)
     ncells = sum(b.ncells for b in wl.boxes)
@@ -443,6 +446,7 @@ def ours(args):
                        "cell_steps_per_step_per_gpu": wl.cell_steps, "fused_calls_per_step": len(wl.calls),
                        "rtol": args.rtol, "atol_Y": args.atol, "atol_T": ATOL_T, "method": args.method,
                        "lanes_per_cell": args.lanes, "temperature_mode": args.tmode, "h0_factor": args.h0,
+                       **({"opts": args.opt} if args.opt else {}),
                        "l2": "inputs >= 369 MB/GPU > 126 MB L2 (no flush needed)",
                        "parallelism": f"boxes over {world} rank(s)", **wl.extra},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
@@ -457,7 +461,9 @@ def ours(args):
                        "active_per_iter": s0["active_per_iter"], "sparse_cells": s0["sparse_cells"],
                        "active0": s0["active0"], "t_gate_ms": s0["t_gate_ms"], "t_compact_ms": s0["t_compact_ms"],
                        "t_sparse_ms": s0["t_sparse_ms"], "n_unfinished": s0["n_unfinished"],
-                       "n_nonfinite": s0["n_nonfinite"], "max_energy_drift": s0["max_energy_drift"]},
+                       "n_nonfinite": s0["n_nonfinite"], "max_energy_drift": s0["max_energy_drift"],
+                       "lockstep": s0["lockstep"],
+                       "bulk_simt_eff": s0["bulk_substeps"] / max(32 * s0["warp_substeps"], 1)},
         }
         print(json.dumps(line))
     if world > 1:

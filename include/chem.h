@@ -99,11 +99,19 @@ typedef struct {
                                cell ends its burst early takes the next id); 0: one thread per id */
     double h0_factor;       /* first substep of a cell = h0_factor * |y|/|f(y)| (WRMS norms), capped
                                at dt (Hairer-Norsett-Wanner I.II.4 use 0.01)                      */
+    int32_t lockstep;       /* bulk bursts run as 224-thread blocks whose warps take every substep
+                               together (one barrier per substep), keeping an SM's warps in the same
+                               code on heterogeneous fields (shared instruction cache):
+                               0 off, 1 on, 2 auto (on while the previous call's bulk SIMT efficiency
+                               = lane substeps / (32 x warp substeps) is below 0.9).  Results are
+                               bitwise independent of this choice.                                */
+    int32_t kmax_first;     /* substeps of the first bulk burst of a lockstep call (1: cells that
+                               finish in one substep leave before the lockstep bursts); 0: kmax_bulk */
 } chem_opts;
 
 /* fills the paper's defaults: 500 K, 5, 1e4, 1e5, 1e-6 K, RODAS4, compact_bulk = 1, lanes_per_cell = 1,
    eps_change = 0.01, temperature_mode = 0,
-   refill_bulk = 0, h0_factor = 0.01 */
+   refill_bulk = 0, h0_factor = 0.01, lockstep = 2 (auto), kmax_first = 1 */
 void chem_default_opts(chem_opts* o);
 
 /* ---- one AMR box / grid (FAB analogue) for the fused multi-box call ----------------- */
@@ -134,6 +142,10 @@ typedef struct {
     double t_gate_ms, t_bulk_ms, t_compact_ms, t_sparse_ms;   /* CUDA-event phase times         */
     double max_energy_drift;    /* max |T_int - T(e, Y_out)| / T over finished cells            */
     int64_t active_per_iter[16];/* N_active after each of the first 16 bulk launches (App. B)   */
+    int64_t warp_substeps;      /* warp-level substep issues in bulk launches (SIMT efficiency =
+                                   bulk lane substeps / (32 x warp_substeps))                   */
+    int64_t bulk_substeps;      /* lane substeps attempted in bulk launches                     */
+    int64_t lockstep;           /* 1: this call's bulk bursts ran in lockstep                   */
 } chem_stats;
 
 typedef struct chem_ctx chem_ctx;   /* opaque, library-owned */

@@ -17,7 +17,8 @@ using namespace chem;
 
 namespace {
 
-constexpr int kIntegrateBS = 32;   // threads per block of k_integrate: 1008 B smem/thread -> 7 blocks/SM
+constexpr int kIntegrateBS = 32;
+constexpr double kLockEff = 0.9;   // chem_opts.lockstep = 2: lockstep while the last bulk SIMT efficiency < 0.9
 constexpr int kStreamBS = 256;     // gate / compaction / box cost
 constexpr int kPointBS = 128;      // point kernels
 struct MechOpsBS { static constexpr int kGrp = 128; };   // threads per block of k_integrate_grp
@@ -40,6 +41,8 @@ struct Ops {
     cudaError_t (*energy)(const void*, int64_t, int64_t, const double*, const double*, double*, cudaStream_t);
     cudaError_t (*integrate)(const void*, int method, int dae, const LaunchCtx&, const uint32_t*, int64_t, int, int,
                              int, int grid, cudaStream_t);
+    cudaError_t (*integrate_lock)(const void*, int method, int dae, const LaunchCtx&, const uint32_t*, int64_t,
+                                  int kmax, int fin, int nsm, cudaStream_t);
     cudaError_t (*integrate_grp)(const void* gtab, int method, int lanes, const LaunchCtx&, const uint32_t*, int64_t,
                                  int, int, int, int grid, cudaStream_t);
     int (*blocks_per_sm)(int method, int dae);
@@ -190,6 +193,42 @@ struct MechOps {
     static constexpr size_t smem() { return (size_t)SmemLayout<M, Meth, DAE>::bytes_per_thread * kIntegrateBS; }
 
     template <class Meth, bool DAE>
+    static constexpr int lock_bs()
+    {
+        constexpr size_t b = SmemLayout<M, Meth, DAE>::bytes_per_thread;
+        return b == 0 ? 224 : (int)std::min<size_t>(224, (227 * 1024 / b) / 32 * 32);
+    }
+    template <class Meth, bool DAE>
+    static cudaError_t launch_lock(const P& p, const LaunchCtx& L, const uint32_t* ids, int64_t n, int kmax, int fin,
+                                   int nsm, cudaStream_t s)
+    {
+        // persistent: one block per SM walks tiles blockIdx.x, blockIdx.x + gridDim.x, ...
+        constexpr int BS = lock_bs<Meth, DAE>();
+        constexpr size_t sm = (size_t)SmemLayout<M, Meth, DAE>::bytes_per_thread * BS;
+        auto kern = k_integrate<M, Meth, BS, DAE, true>;
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        if (e != cudaSuccess) return e;
+        const int grid = (int)std::min<int64_t>((n + BS - 1) / BS, nsm);
+        kern<<<grid, BS, sm, s>>>(p, L, ids, n, kmax, 0, fin);
+        return cudaGetLastError();
+    }
+    template <bool DAE>
+    static cudaError_t lock_t(const P& p, int method, const LaunchCtx& L, const uint32_t* ids, int64_t n, int kmax,
+                              int fin, int nsm, cudaStream_t s)
+    {
+        if (method == CHEM_METHOD_RODAS3) return launch_lock<Rodas3, DAE>(p, L, ids, n, kmax, fin, nsm, s);
+        if (method == CHEM_METHOD_ROS4) return launch_lock<Ros4, DAE>(p, L, ids, n, kmax, fin, nsm, s);
+        return launch_lock<Rodas4, DAE>(p, L, ids, n, kmax, fin, nsm, s);
+    }
+    // lockstep bulk launch (chem_opts.lockstep); Rosenbrock methods only
+    static cudaError_t integrate_lock(const void* pp, int method, int dae, const LaunchCtx& L, const uint32_t* ids,
+                                      int64_t n, int kmax, int fin, int nsm, cudaStream_t s)
+    {
+        const P& p = *static_cast<const P*>(pp);
+        return dae ? lock_t<true>(p, method, L, ids, n, kmax, fin, nsm, s)
+                   : lock_t<false>(p, method, L, ids, n, kmax, fin, nsm, s);
+    }
+    template <class Meth, bool DAE>
     static cudaError_t launch(const P& p, const LaunchCtx& L, const uint32_t* ids, int64_t n, int kmax, int refill,
                               int fin, int grid, cudaStream_t s)
     {
@@ -298,6 +337,7 @@ struct MechOps {
         o.temperature = &temperature;
         o.energy = &energy;
         o.integrate = &integrate;
+        o.integrate_lock = &integrate_lock;
         o.blocks_per_sm = &blocks_per_sm;
         o.integrate_grp = &integrate_grp;
         o.grp_blocks_per_sm = &grp_blocks_per_sm;
@@ -402,6 +442,7 @@ struct chem_ctx {
     bool grp_ok = false;             // the group kernel needs one shared NASA T_mid
     int32_t* trace = nullptr;        // device [trace_rows][nboxes] activity trace (App. B), or null
     int32_t trace_rows = 0;
+    double simt_eff = 1.0;           // bulk SIMT efficiency of the last call (lockstep = 2 input)
 };
 
 namespace {
@@ -454,6 +495,8 @@ void chem_default_opts(chem_opts* o)
     o->temperature_mode = 0;
     o->refill_bulk = 0;
     o->h0_factor = 0.01;
+    o->lockstep = 2;
+    o->kmax_first = 1;
 }
 
 const char* chem_strerror(int code)
@@ -475,6 +518,7 @@ static int check_opts(const chem_opts* o)
         (o->method < CHEM_METHOD_RODAS4 || o->method > CHEM_METHOD_ROS4) ||
         !std::isfinite(o->T_min) || !(o->eps_change > 0.0 && o->eps_change <= 1.0) ||
         (o->temperature_mode != 0 && o->temperature_mode != 1) || (o->refill_bulk != 0 && o->refill_bulk != 1) ||
+        o->lockstep < 0 || o->lockstep > 2 || o->kmax_first < 0 ||
         !(o->h0_factor > 0.0 && o->h0_factor <= 1.0) ||
         (o->lanes_per_cell != 1 && o->lanes_per_cell != 4 && o->lanes_per_cell != 8))
         return CHEM_EINVAL;
@@ -701,8 +745,7 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
     }
 
     auto read_count = [&](int64_t& v) -> cudaError_t {
-        cudaError_t r = cudaMemcpyAsync(c->h_stats + S_COUNT_ACTIVE, L.stats + S_COUNT_ACTIVE, 8,
-                                        cudaMemcpyDeviceToHost, s);
+        cudaError_t r = cudaMemcpyAsync(c->h_stats, L.stats, S_NSTATS * 8, cudaMemcpyDeviceToHost, s);
         if (r != cudaSuccess) return r;
         r = cudaStreamSynchronize(s);
         v = (int64_t)c->h_stats[S_COUNT_ACTIVE];
@@ -734,22 +777,32 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
     const uint32_t* cur = ids0;
     int64_t n_cur = n_active;
     uint32_t* nxt = idsA;
+    // lockstep bursts (chem_opts.lockstep; auto: the previous call's bulk SIMT efficiency was low)
+    const bool lock = !use_grp && !o.refill_bulk && o.method != CHEM_METHOD_EXPLICIT &&
+                      (o.lockstep == 1 || (o.lockstep == 2 && c->simt_eff < kLockEff));
+    st.lockstep = lock;
+    unsigned long long att_skip = 0, ws_skip = 0;   // the one-substep first burst is not a SIMT sample
     while (n_cur > o.n_active_star && n_cur > 0) {
+        const bool first_burst = lock && st.bulk_iters == 0 && o.kmax_first > 0;
+        const int kmax_b = first_burst ? o.kmax_first : o.kmax_bulk;
         const bool all_cells = !o.compact_bulk;
         const uint32_t* lst = all_cells ? nullptr : cur;
         const int64_t nl = all_cells ? total : n_cur;
         CK(cudaEventRecord(c->ev[0], s));
         if (use_grp)
-            CK(ops.integrate_grp(c->d_gtab, o.method, o.lanes_per_cell, L, lst, nl, o.kmax_bulk, 0, 0,
+            CK(ops.integrate_grp(c->d_gtab, o.method, o.lanes_per_cell, L, lst, nl, kmax_b, 0, 0,
                                  (int)((nl * o.lanes_per_cell + MechOpsBS::kGrp - 1) / MechOpsBS::kGrp), s));
+        else if (lock)
+            CK(ops.integrate_lock(c->params.data(), o.method, o.temperature_mode, L, lst, nl, kmax_b, 0, c->num_sms,
+                                  s));
         else if (o.refill_bulk) {
             // persistent grid; a lane whose cell finishes its burst early takes the next id
             CK(cudaMemsetAsync(L.stats + S_CURSOR, 0, 8, s));
             const int grid = std::max(1, std::min<int>(c->num_sms * ops.blocks_per_sm(o.method, o.temperature_mode),
                                                        (int)((nl + kIntegrateBS - 1) / kIntegrateBS)));
-            CK(ops.integrate(c->params.data(), o.method, o.temperature_mode, L, lst, nl, o.kmax_bulk, 1, 0, grid, s));
+            CK(ops.integrate(c->params.data(), o.method, o.temperature_mode, L, lst, nl, kmax_b, 1, 0, grid, s));
         } else
-            CK(ops.integrate(c->params.data(), o.method, o.temperature_mode, L, lst, nl, o.kmax_bulk, 0, 0,
+            CK(ops.integrate(c->params.data(), o.method, o.temperature_mode, L, lst, nl, kmax_b, 0, 0,
                              (int)((nl + kIntegrateBS - 1) / kIntegrateBS), s));
         CK(cudaEventRecord(c->ev[1], s));
         CK(cudaEventSynchronize(c->ev[1]));
@@ -761,6 +814,10 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
         CK(cudaEventRecord(c->ev[1], s));
         CK(read_count(n_cur));
         st.t_compact_ms += elapsed(c);
+        if (first_burst) {
+            att_skip = c->h_stats[S_ATTEMPTED];
+            ws_skip = c->h_stats[S_WARP_SUBSTEPS];
+        }
         if (st.bulk_iters < 16) st.active_per_iter[st.bulk_iters] = n_cur;
         st.bulk_iters++;
         if (tracing && st.bulk_iters < c->trace_rows && n_cur > 0) {
@@ -770,6 +827,13 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
         }
         cur = nxt;
         nxt = (nxt == idsA) ? idsB : idsA;
+    }
+
+    if (st.bulk_iters > 0) {
+        st.bulk_substeps = (int64_t)c->h_stats[S_ATTEMPTED];
+        st.warp_substeps = (int64_t)c->h_stats[S_WARP_SUBSTEPS];
+        const unsigned long long ws = c->h_stats[S_WARP_SUBSTEPS] - ws_skip;
+        if (ws > 0) c->simt_eff = (double)(c->h_stats[S_ATTEMPTED] - att_skip) / (32.0 * (double)ws);
     }
 
     // ---- Alg. 3 §3: sparse integration over the index map (persistent, lane refill)

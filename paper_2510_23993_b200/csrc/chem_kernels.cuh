@@ -27,7 +27,7 @@ enum CellState : uint8_t {
 
 enum StatIdx {
     S_ATTEMPTED = 0, S_ACCEPTED, S_RHS, S_JAC, S_LU, S_NEWTON_FAIL, S_NONFINITE, S_TRANGE, S_UNFINISHED,
-    S_DONE, S_DRIFT_BITS, S_COUNT_ACTIVE, S_CURSOR, S_FROZEN, S_NSTATS
+    S_DONE, S_DRIFT_BITS, S_COUNT_ACTIVE, S_CURSOR, S_FROZEN, S_WARP_SUBSTEPS, S_NSTATS
 };
 
 struct DevBox {
@@ -194,7 +194,7 @@ struct SmemLayout {
 
 struct Counters {
     unsigned attempted = 0, accepted = 0, rhs = 0, newton_fail = 0, nonfinite = 0, trange = 0, unfinished = 0,
-             done = 0, frozen = 0;
+             done = 0, frozen = 0, warp_substeps = 0;
     double drift = 0.0;
 };
 
@@ -500,6 +500,7 @@ __device__ __forceinline__ void flush_counters(const LaunchCtx& L, Counters& c)
     warp_add(&L.stats[S_JAC], c.attempted);              // one Jacobian per attempted substep
     warp_add(&L.stats[S_LU], c.attempted - c.frozen);    // one LU per attempted Rosenbrock substep
     warp_add(&L.stats[S_FROZEN], c.frozen);
+    warp_add(&L.stats[S_WARP_SUBSTEPS], c.warp_substeps);
     warp_add(&L.stats[S_NEWTON_FAIL], c.newton_fail);
     warp_add(&L.stats[S_NONFINITE], c.nonfinite);
     warp_add(&L.stats[S_TRANGE], c.trange);
@@ -519,7 +520,10 @@ __device__ __forceinline__ void flush_counters(const LaunchCtx& L, Counters& c)
 // all-cells launch) and runs <= kmax attempted substeps.  Sparse (refill = true): persistent
 // grid; each lane pulls ids from the atomic cursor S_CURSOR until the list is exhausted.
 // Both modes run the same substep code, so results are bitwise independent of K_max and N*.
-template <class M, class Meth, int BS, bool DAE = false>
+// LOCK: the block's warps take each substep together (one __syncthreads_or per substep), so that on a
+// heterogeneous field the SM's resident warps stay in the same code region (shared instruction cache)
+// instead of drifting apart; a thread whose cell has left the burst idles at the barrier.
+template <class M, class Meth, int BS, bool DAE = false, bool LOCK = false>
 __global__ void __launch_bounds__(BS) k_integrate(const __grid_constant__ Params<M> P, LaunchCtx L,
                                                   const uint32_t* __restrict__ ids, int64_t n_ids, int kmax,
                                                   int refill, int final_phase)
@@ -534,17 +538,22 @@ __global__ void __launch_bounds__(BS) k_integrate(const __grid_constant__ Params
     Counters cnt;
     Cell<M> C;
     bool have = false;
+    bool live = true;     // this thread may still take a cell
     bool first = true;
+    int64_t tile = blockIdx.x;
     for (;;) {
-        if (!have) {
+        while (!have && live) {
             int64_t idx;
             if (refill) {
                 idx = (int64_t)atomicAdd(&L.stats[S_CURSOR], 1ull);
+            } else if (LOCK) {
+                idx = first ? tile * BS + threadIdx.x : n_ids;   // persistent: tiles blockIdx.x + k*gridDim.x
+                first = false;
             } else {
                 idx = first ? (int64_t)blockIdx.x * BS + threadIdx.x : n_ids;
                 first = false;
             }
-            if (idx >= n_ids) break;
+            if (idx >= n_ids) { live = false; break; }
             const uint32_t g = ids ? ids[idx] : (uint32_t)idx;
             const uint8_t st = L.state[g];
             if ((st & 0x7f) != ST_FRESH && (st & 0x7f) != ST_RUNNING) continue;
@@ -552,6 +561,21 @@ __global__ void __launch_bounds__(BS) k_integrate(const __grid_constant__ Params
             load_cell<M>(P, L, g, C, st, cnt, ok);
             if (!ok) { L.state[g] = ST_FAILED; continue; }
             have = true;
+        }
+        if constexpr (LOCK) {
+            if (!__syncthreads_or(have)) {
+                if (refill) break;
+                tile += gridDim.x;                  // block-uniform: next tile of this persistent block
+                if (tile * BS >= n_ids) break;
+                first = true;
+                live = true;
+                continue;
+            }
+            if (!have) continue;
+        } else if (!have) break;
+        {   // SIMT efficiency statistic: the lowest lane executing this substep counts one warp substep
+            const unsigned am = __activemask();
+            if ((int)(threadIdx.x & 31) == __ffs(am) - 1) cnt.warp_substeps++;
         }
         int r;
         if constexpr (Meth::S == 0) r = explicit_step<M>(P, L, C, L.eps_change, cnt);

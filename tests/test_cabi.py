@@ -45,6 +45,21 @@ def test_default_opts_are_the_papers():
     from paper_2510_23993_b200 import binding
     o = binding.default_opts()
     assert (o.kmax_bulk, o.n_active_star, o.kmax_sparse, o.T_min) == (5, 10000, 100000, 500.0)
+    assert (o.lockstep, o.kmax_first, o.refill_bulk, o.compact_bulk) == (2, 1, 0, 1)
+
+
+def test_opts_struct_matches_header():
+    """The ctypes mirrors list the header's chem_opts / chem_stats fields in order (a missed field
+    would shift every later one)."""
+    import pathlib
+    from paper_2510_23993_b200 import binding
+    hdr = (pathlib.Path(__file__).resolve().parent.parent / "include" / "chem.h").read_text()
+    for struct, cls in (("chem_opts", binding.ChemOpts), ("chem_stats", binding.ChemStats)):
+        body = hdr[:hdr.index("} " + struct + ";")]
+        body = body[body.rindex("typedef struct {"):]
+        body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+        names = re.findall(r"\b(\w+)(?:\[\d+\])?\s*[,;]", body)
+        assert names == [n for n, _ in cls._fields_], (struct, names)
 
 
 def test_init_rejects_unbalanced_mechanism_without_gpu():

@@ -188,15 +188,17 @@ def test_virtual_ranks_bitwise(chem, ora, doc):
 
 
 @pytest.mark.parametrize("opts", [dict(refill_bulk=1), dict(kmax_bulk=20, n_active_star=3000),
-                                  dict(compact_bulk=0, kmax_bulk=3)])
+                                  dict(compact_bulk=0, kmax_bulk=3), dict(lockstep=1),
+                                  dict(lockstep=1, kmax_first=0, kmax_bulk=3), dict(lockstep=1, compact_bulk=0)])
 def test_cfg3_schedule_variants_bitwise(ora, doc, opts):
     """Bulk-sparse variants (lane-refill bursts, longer bursts, the paper's all-cells bursts) give
     bitwise the same field as the default schedule (P:177 / S:191), at full cfg3 size."""
     m = ora.m
     ids = [0, 16, 32, 48]                    # the four boxes along y at x = 0 (band + spots)
     raw, _ = synth.field_cfg3(doc, m.W, m.species, device=DEV, box_ids=ids)
-    ref, st0, _ = _run(Chem("h2air_li2004", device=0, atol_T=1e-6), raw)
+    ref, st0, _ = _run(Chem("h2air_li2004", device=0, atol_T=1e-6, lockstep=0), raw)
     alt, st1, _ = _run(Chem("h2air_li2004", device=0, atol_T=1e-6, **opts), raw)
+    assert st1["lockstep"] == opts.get("lockstep", 0)
     for a, b in zip(ref, alt):
         assert torch.equal(a.T, b.T) and torch.equal(a.Y, b.Y)
     assert st0["steps_attempted"] == st1["steps_attempted"]
