@@ -12,16 +12,15 @@
 
 #include "../../include/chem.h"
 #include "chem_group.cuh"
+#include "chem_launch.cuh"
 
 using namespace chem;
 
 namespace {
 
-constexpr int kIntegrateBS = 32;
 constexpr double kLockEff = 0.9;   // chem_opts.lockstep = 2: lockstep while the last bulk SIMT efficiency < 0.9
 constexpr int kStreamBS = 256;     // gate / compaction / box cost
 constexpr int kPointBS = 128;      // point kernels
-struct MechOpsBS { static constexpr int kGrp = 128; };   // threads per block of k_integrate_grp
 
 // ------------------------------------------------------------------ per-structure operations
 struct Ops {
@@ -189,36 +188,14 @@ struct MechOps {
         return cudaGetLastError();
     }
 
-    template <class Meth, bool DAE = false>
-    static constexpr size_t smem() { return (size_t)SmemLayout<M, Meth, DAE>::bytes_per_thread * kIntegrateBS; }
-
-    template <class Meth, bool DAE>
-    static constexpr int lock_bs()
-    {
-        constexpr size_t b = SmemLayout<M, Meth, DAE>::bytes_per_thread;
-        return b == 0 ? 224 : (int)std::min<size_t>(224, (227 * 1024 / b) / 32 * 32);
-    }
-    template <class Meth, bool DAE>
-    static cudaError_t launch_lock(const P& p, const LaunchCtx& L, const uint32_t* ids, int64_t n, int kmax, int fin,
-                                   int nsm, cudaStream_t s)
-    {
-        // persistent: one block per SM walks tiles blockIdx.x, blockIdx.x + gridDim.x, ...
-        constexpr int BS = lock_bs<Meth, DAE>();
-        constexpr size_t sm = (size_t)SmemLayout<M, Meth, DAE>::bytes_per_thread * BS;
-        auto kern = k_integrate<M, Meth, BS, DAE, true>;
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        if (e != cudaSuccess) return e;
-        const int grid = (int)std::min<int64_t>((n + BS - 1) / BS, nsm);
-        kern<<<grid, BS, sm, s>>>(p, L, ids, n, kmax, 0, fin);
-        return cudaGetLastError();
-    }
+    // ---- integration launchers (defined in chem_launch_impl.cuh, instantiated in launch_*.cu)
     template <bool DAE>
     static cudaError_t lock_t(const P& p, int method, const LaunchCtx& L, const uint32_t* ids, int64_t n, int kmax,
                               int fin, int nsm, cudaStream_t s)
     {
-        if (method == CHEM_METHOD_RODAS3) return launch_lock<Rodas3, DAE>(p, L, ids, n, kmax, fin, nsm, s);
-        if (method == CHEM_METHOD_ROS4) return launch_lock<Ros4, DAE>(p, L, ids, n, kmax, fin, nsm, s);
-        return launch_lock<Rodas4, DAE>(p, L, ids, n, kmax, fin, nsm, s);
+        if (method == CHEM_METHOD_RODAS3) return Launch<M, Rodas3, DAE>::lock(p, L, ids, n, kmax, fin, nsm, s);
+        if (method == CHEM_METHOD_ROS4) return Launch<M, Ros4, DAE>::lock(p, L, ids, n, kmax, fin, nsm, s);
+        return Launch<M, Rodas4, DAE>::lock(p, L, ids, n, kmax, fin, nsm, s);
     }
     // lockstep bulk launch (chem_opts.lockstep); Rosenbrock methods only
     static cudaError_t integrate_lock(const void* pp, int method, int dae, const LaunchCtx& L, const uint32_t* ids,
@@ -228,26 +205,14 @@ struct MechOps {
         return dae ? lock_t<true>(p, method, L, ids, n, kmax, fin, nsm, s)
                    : lock_t<false>(p, method, L, ids, n, kmax, fin, nsm, s);
     }
-    template <class Meth, bool DAE>
-    static cudaError_t launch(const P& p, const LaunchCtx& L, const uint32_t* ids, int64_t n, int kmax, int refill,
-                              int fin, int grid, cudaStream_t s)
-    {
-        auto kern = k_integrate<M, Meth, kIntegrateBS, DAE>;
-        cudaError_t e = cudaSuccess;
-        if (smem<Meth, DAE>() > 0)
-            e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem<Meth, DAE>());
-        if (e != cudaSuccess) return e;
-        kern<<<grid, kIntegrateBS, smem<Meth, DAE>(), s>>>(p, L, ids, n, kmax, refill, fin);
-        return cudaGetLastError();
-    }
     template <bool DAE>
     static cudaError_t integrate_t(const P& p, int method, const LaunchCtx& L, const uint32_t* ids, int64_t n,
                                    int kmax, int refill, int fin, int grid, cudaStream_t s)
     {
-        if (method == CHEM_METHOD_RODAS3) return launch<Rodas3, DAE>(p, L, ids, n, kmax, refill, fin, grid, s);
-        if (method == CHEM_METHOD_EXPLICIT) return launch<Explicit, false>(p, L, ids, n, kmax, refill, fin, grid, s);
-        if (method == CHEM_METHOD_ROS4) return launch<Ros4, DAE>(p, L, ids, n, kmax, refill, fin, grid, s);
-        return launch<Rodas4, DAE>(p, L, ids, n, kmax, refill, fin, grid, s);
+        if (method == CHEM_METHOD_RODAS3) return Launch<M, Rodas3, DAE>::run(p, L, ids, n, kmax, refill, fin, grid, s);
+        if (method == CHEM_METHOD_EXPLICIT) return Launch<M, Explicit, false>::run(p, L, ids, n, kmax, refill, fin, grid, s);
+        if (method == CHEM_METHOD_ROS4) return Launch<M, Ros4, DAE>::run(p, L, ids, n, kmax, refill, fin, grid, s);
+        return Launch<M, Rodas4, DAE>::run(p, L, ids, n, kmax, refill, fin, grid, s);
     }
     static cudaError_t integrate(const void* pp, int method, int dae, const LaunchCtx& L, const uint32_t* ids,
                                  int64_t n, int kmax, int refill, int fin, int grid, cudaStream_t s)
@@ -256,65 +221,34 @@ struct MechOps {
         return dae ? integrate_t<true>(p, method, L, ids, n, kmax, refill, fin, grid, s)
                    : integrate_t<false>(p, method, L, ids, n, kmax, refill, fin, grid, s);
     }
-    template <class Meth, bool DAE>
-    static int bps()
-    {
-        int nb = 0;
-        auto kern = k_integrate<M, Meth, kIntegrateBS, DAE>;
-        if (smem<Meth, DAE>() > 0)
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem<Meth, DAE>());
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kIntegrateBS, smem<Meth, DAE>());
-        return std::max(nb, 1);
-    }
     static int blocks_per_sm(int method, int dae)
     {
-        if (method == CHEM_METHOD_EXPLICIT) return bps<Explicit, false>();
+        if (method == CHEM_METHOD_EXPLICIT) return Launch<M, Explicit, false>::blocks_per_sm();
         if (dae) {
-            if (method == CHEM_METHOD_RODAS3) return bps<Rodas3, true>();
-            if (method == CHEM_METHOD_ROS4) return bps<Ros4, true>();
-            return bps<Rodas4, true>();
+            if (method == CHEM_METHOD_RODAS3) return Launch<M, Rodas3, true>::blocks_per_sm();
+            if (method == CHEM_METHOD_ROS4) return Launch<M, Ros4, true>::blocks_per_sm();
+            return Launch<M, Rodas4, true>::blocks_per_sm();
         }
-        if (method == CHEM_METHOD_RODAS3) return bps<Rodas3, false>();
-        if (method == CHEM_METHOD_ROS4) return bps<Ros4, false>();
-        return bps<Rodas4, false>();
+        if (method == CHEM_METHOD_RODAS3) return Launch<M, Rodas3, false>::blocks_per_sm();
+        if (method == CHEM_METHOD_ROS4) return Launch<M, Ros4, false>::blocks_per_sm();
+        return Launch<M, Rodas4, false>::blocks_per_sm();
     }
 
     // ---- lane-group kernel
-    static constexpr int kGrpBS = MechOpsBS::kGrp;
-    template <class Meth, int G>
-    static cudaError_t launch_grp(const void* gt, const LaunchCtx& L, const uint32_t* ids, int64_t n, int kmax,
-                                  int refill, int fin, int grid, cudaStream_t s)
-    {
-        auto kern = k_integrate_grp<M, Meth, G, kGrpBS>;
-        const size_t sm = grp_smem_bytes<M, G>(kGrpBS);
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        if (e != cudaSuccess) return e;
-        kern<<<grid, kGrpBS, sm, s>>>(static_cast<const GTable<M>*>(gt), L, ids, n, kmax, refill, fin);
-        return cudaGetLastError();
-    }
     static cudaError_t integrate_grp(const void* gt, int method, int lanes, const LaunchCtx& L, const uint32_t* ids,
                                      int64_t n, int kmax, int refill, int fin, int grid, cudaStream_t s)
     {
         if (method == CHEM_METHOD_RODAS3)
-            return lanes == 4 ? launch_grp<Rodas3, 4>(gt, L, ids, n, kmax, refill, fin, grid, s)
-                              : launch_grp<Rodas3, 8>(gt, L, ids, n, kmax, refill, fin, grid, s);
-        return lanes == 4 ? launch_grp<Rodas4, 4>(gt, L, ids, n, kmax, refill, fin, grid, s)
-                          : launch_grp<Rodas4, 8>(gt, L, ids, n, kmax, refill, fin, grid, s);
-    }
-    template <class Meth, int G>
-    static int gbps()
-    {
-        int nb = 0;
-        auto kern = k_integrate_grp<M, Meth, G, kGrpBS>;
-        const size_t sm = grp_smem_bytes<M, G>(kGrpBS);
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kGrpBS, sm);
-        return std::max(nb, 1);
+            return lanes == 4 ? LaunchGrp<M, Rodas3, 4>::run(gt, L, ids, n, kmax, refill, fin, grid, s)
+                              : LaunchGrp<M, Rodas3, 8>::run(gt, L, ids, n, kmax, refill, fin, grid, s);
+        return lanes == 4 ? LaunchGrp<M, Rodas4, 4>::run(gt, L, ids, n, kmax, refill, fin, grid, s)
+                          : LaunchGrp<M, Rodas4, 8>::run(gt, L, ids, n, kmax, refill, fin, grid, s);
     }
     static int grp_blocks_per_sm(int method, int lanes)
     {
-        if (method == CHEM_METHOD_RODAS3) return lanes == 4 ? gbps<Rodas3, 4>() : gbps<Rodas3, 8>();
-        return lanes == 4 ? gbps<Rodas4, 4>() : gbps<Rodas4, 8>();
+        if (method == CHEM_METHOD_RODAS3)
+            return lanes == 4 ? LaunchGrp<M, Rodas3, 4>::blocks_per_sm() : LaunchGrp<M, Rodas3, 8>::blocks_per_sm();
+        return lanes == 4 ? LaunchGrp<M, Rodas4, 4>::blocks_per_sm() : LaunchGrp<M, Rodas4, 8>::blocks_per_sm();
     }
     static void build_gtab(const void* params, void* out)
     {
@@ -343,7 +277,7 @@ struct MechOps {
         o.grp_blocks_per_sm = &grp_blocks_per_sm;
         o.gtab_size = sizeof(GTable<M>);
         o.build_gtab = &build_gtab;
-        o.integrate_smem = smem<Rodas4, false>();
+        o.integrate_smem = Launch<M, Rodas4, false>::smem();
         return o;
     }
 };
@@ -791,7 +725,7 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
         CK(cudaEventRecord(c->ev[0], s));
         if (use_grp)
             CK(ops.integrate_grp(c->d_gtab, o.method, o.lanes_per_cell, L, lst, nl, kmax_b, 0, 0,
-                                 (int)((nl * o.lanes_per_cell + MechOpsBS::kGrp - 1) / MechOpsBS::kGrp), s));
+                                 (int)((nl * o.lanes_per_cell + kGrpBS - 1) / kGrpBS), s));
         else if (lock)
             CK(ops.integrate_lock(c->params.data(), o.method, o.temperature_mode, L, lst, nl, kmax_b, 0, c->num_sms,
                                   s));
@@ -842,7 +776,7 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
         CK(cudaMemsetAsync(L.stats + S_CURSOR, 0, 8, s));
         CK(cudaEventRecord(c->ev[0], s));
         if (use_grp) {
-            const int cells_per_block = MechOpsBS::kGrp / o.lanes_per_cell;
+            const int cells_per_block = kGrpBS / o.lanes_per_cell;
             const int grid = std::max(1, std::min<int>(c->num_sms * ops.grp_blocks_per_sm(o.method, o.lanes_per_cell),
                                                        (int)((n_cur + cells_per_block - 1) / cells_per_block)));
             CK(ops.integrate_grp(c->d_gtab, o.method, o.lanes_per_cell, L, cur, n_cur, o.kmax_sparse, 1, 1, grid, s));

@@ -11,6 +11,8 @@
 // RODAS4/RODAS3 with the same controller); reductions across lanes run in a fixed order, so a cell's
 // result is deterministic and independent of K_max, N*, box grouping and scheduling.
 #pragma once
+#include <cstring>
+
 #include "chem_kernels.cuh"
 
 namespace chem {
@@ -169,11 +171,11 @@ __device__ __forceinline__ double g_troe(const R& x, double T, double invT, doub
             Fc += e2;
             dFc += x.tT2 * invT * invT * e2;
         }
-        L = log(Fc) * kLog10e;
+        L = flog(Fc) * kLog10e;
     }
     const double C = -0.4 - 0.67 * L;
     const double N = 0.75 - 1.27 * L;
-    const double xx = log(fmax(Pr, 1e-300)) * kLog10e;
+    const double xx = flog(fmax(Pr, 1e-300)) * kLog10e;
     const double u = xx + C;
     const double den = N - 0.14 * u;
     const double f1 = u / den;
@@ -221,7 +223,7 @@ __device__ __forceinline__ void g_rhs(const GTable<M>& tb, const Grp<G>& gr, dou
     }
     gr.sync();
     const double T = cs[LY::oT];
-    const double lnT = log(T);
+    const double lnT = flog(T);
     const double invT = 1.0 / T;
     const double RT = tb.R * T;
     // 2. species phase: thermo, c, ln c; partial sums of cv, dcv/dT, [M]
@@ -234,7 +236,7 @@ __device__ __forceinline__ void g_rhs(const GTable<M>& tb, const Grp<G>& gr, dou
             g_thermo<M>(tb, k, T, lnT, invT, cpR, hRT, sR, dcpR);
             const double Yk = cs[LY::oY + k];
             const double c = rho * fmax(Yk, 0.0) * tb.invW[k];
-            cs[LY::oLnc + k] = log(c);
+            cs[LY::oLnc + k] = flog(c);
             cs[LY::oC + k] = c;
             cs[LY::oG + k] = hRT - sR;
             cs[LY::oH + k] = hRT;

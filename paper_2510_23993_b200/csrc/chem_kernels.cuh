@@ -673,7 +673,7 @@ __global__ void k_temperature(const __grid_constant__ Params<M> P, int64_t n, in
 // PAPER.md Alg. 1: internal energy from the conserved variables, column-major
 // U[c*ld + i], c = rho, rho u_x, rho u_y, rho u_z, rho E:  e = rho E/rho - (u_x^2 + u_y^2 + u_z^2)/2.
 // The caller-side step before chemistry (NEXT-4); HBM-bound (40 B in, 8 B out per cell).
-__global__ void k_internal_energy(int64_t n, int64_t ld, const double* __restrict__ U, double* __restrict__ e)
+static __global__ void k_internal_energy(int64_t n, int64_t ld, const double* __restrict__ U, double* __restrict__ e)
 {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const double rho = U[i];
