@@ -186,7 +186,8 @@ template <class M, class Meth, bool DAE = false>
 struct SmemLayout {
     static constexpr int n = DAE ? M::NSA : M::NSA + 1;
     static constexpr bool none = (Meth::S == 0);   // explicit scheme: no matrix, no stages
-    static constexpr int nK = Meth::stiff_last ? Meth::S - 1 : Meth::S;
+    // stage slots: RODAS4 keeps three (ros_step's collapse), stiffly accurate methods S-1, others S
+    static constexpr int nK = Meth::collapse ? 3 : (Meth::stiff_last ? Meth::S - 1 : Meth::S);
     static constexpr int off_K = none ? 0 : n * n;
     static constexpr int doubles = none ? 0 : n * n + nK * n;   // pivots are kept in registers
     static constexpr int bytes_per_thread = doubles * 8;
@@ -272,37 +273,54 @@ __device__ __forceinline__ int ros_step(const Params<M>& P, const LaunchCtx& L, 
     for (int i = 0; i < n; ++i)
 #pragma unroll
         for (int j = 0; j < n; ++j) A(i, j) = (i == j) ? ghinv - A(i, j) : -A(i, j);
-    uint64_t piv[(n + 7) / 8];
-    const bool ok = lu_factor<n>(A, piv);
+    uint64_t perm;
+    const bool ok = lu_factor<n>(A, perm);
 
     const double hinv = 1.0 / h;
-    double Flast[Meth::reuse_last ? n : 1];   // f of the last new stage point (methods reusing it)
-    double ylast[n];                          // stage point of the last stage (stiffly accurate)
-    double xlast[n];                          // K of the last stage (not stored when stiff_last)
-    {   // stage 0: K_0 = A^{-1} f(y)
-        double x[n];
-#pragma unroll
-        for (int i = 0; i < n; ++i) Ks[i * ss] = f0[i];
-        if constexpr (Meth::reuse_last) {
-#pragma unroll
-            for (int i = 0; i < n; ++i) Flast[i] = f0[i];
-        }
-        lu_solve<n>(A, piv, Ks, ss, x);
-    }
     bool stage_ok = true;
+    double ylast[n];                          // stage point of the last stage (stiffly accurate)
+    auto slot = [&](int j) { return Ks + (j * n) * ss; };
+    if constexpr (Meth::collapse) {
+        // RODAS4 in three stage slots S0..S2.  Stages 1-3 read the raw K_0..K_2; after stage 3's
+        // point and correction are formed, the slots are collapsed in place into the partial sums
+        // stages 4-5 need (a_5j = a_4j for j < 4, a_54 = 1; stiffly accurate):
+        //   S0 = sum_j a_4j K_j,  S1 = sum_j c_4j K_j,  S2 = sum_j c_5j K_j   (j < 3)
+        // and every later K_s is scatter-added into them (K_3 into all three, K_4 into S0 with
+        // a_54 = 1 and into S2).  Stage 4 reads (S0, S1), stage 5 reads (S0, S2) and K_5 lands in
+        // the free S1.  Same sums as the textbook form, different rounding order.
+        {
+            double x[n];
+#pragma unroll
+            for (int i = 0; i < n; ++i) x[i] = f0[i];
+            lu_solve<n>(A, x);
+            scatter_perm<n>(perm, x, slot(0), ss);
+        }
 #pragma unroll 1
-    for (int s = 1; s < S; ++s) {
-        double F[n];
-        double ys[n];
+        for (int s = 1; s < S; ++s) {
+            double F[n];
+            double ys[n];
+            double G[n];
+            if (s <= 3) {
 #pragma unroll
-        for (int i = 0; i < n; ++i) ys[i] = C.y[i];
-        if (!Meth::reuse_last || Meth::newf_rt(s)) {
+                for (int i = 0; i < n; ++i) { ys[i] = C.y[i]; G[i] = 0.0; }
 #pragma unroll
-            for (int j = 0; j < S - 1; ++j) {
-                if (j < s) {
-                    const double a = Meth::a_rt(s, j);
+                for (int j = 0; j < 3; ++j) {
+                    if (j < s) {
+                        const double a = Meth::a_rt(s, j), c = Meth::c_rt(s, j);
 #pragma unroll
-                    for (int i = 0; i < n; ++i) ys[i] = fma(a, Ks[(j * n + i) * ss], ys[i]);
+                        for (int i = 0; i < n; ++i) {
+                            const double kj = slot(j)[i * ss];
+                            ys[i] = fma(a, kj, ys[i]);
+                            G[i] = fma(c, kj, G[i]);
+                        }
+                    }
+                }
+            } else {
+                const double* gs = slot(s == 4 ? 1 : 2);
+#pragma unroll
+                for (int i = 0; i < n; ++i) {
+                    ys[i] = C.y[i] + slot(0)[i * ss];
+                    G[i] = gs[i * ss];
                 }
             }
             if constexpr (DAE) {
@@ -312,33 +330,97 @@ __device__ __forceinline__ int ros_step(const Params<M>& P, const LaunchCtx& L, 
                 rhs<M>(P, C.rho, invrho, ys, C.Yin, F);
             }
             cnt.rhs++;
+#pragma unroll
+            for (int i = 0; i < n; ++i) F[i] = fma(hinv, G[i], F[i]);
+            if (s == 3) {
+                // collapse (K_0, K_1, K_2) -> (sum a_4j K_j, sum c_4j K_j, sum c_5j K_j), j < 3
+                const double a0 = Meth::a_rt(4, 0), a1 = Meth::a_rt(4, 1), a2 = Meth::a_rt(4, 2);
+                const double c0 = Meth::c_rt(4, 0), c1 = Meth::c_rt(4, 1), c2 = Meth::c_rt(4, 2);
+                const double d0 = Meth::c_rt(5, 0), d1 = Meth::c_rt(5, 1), d2 = Meth::c_rt(5, 2);
+#pragma unroll
+                for (int i = 0; i < n; ++i) {
+                    const double k0 = slot(0)[i * ss], k1 = slot(1)[i * ss], k2 = slot(2)[i * ss];
+                    slot(0)[i * ss] = fma(a2, k2, fma(a1, k1, a0 * k0));
+                    slot(1)[i * ss] = fma(c2, k2, fma(c1, k1, c0 * k0));
+                    slot(2)[i * ss] = fma(d2, k2, fma(d1, k1, d0 * k0));
+                }
+            }
+            lu_solve<n>(A, F);
+            if (s < 3) {
+                scatter_perm<n>(perm, F, slot(s), ss);
+            } else if (s == 3) {
+                scatter_perm<n, true>(perm, F, slot(0), ss, Meth::a_rt(4, 3));
+                scatter_perm<n, true>(perm, F, slot(1), ss, Meth::c_rt(4, 3));
+                scatter_perm<n, true>(perm, F, slot(2), ss, Meth::c_rt(5, 3));
+            } else if (s == 4) {
+                scatter_perm<n, true>(perm, F, slot(0), ss, Meth::a_rt(5, 4));
+                scatter_perm<n, true>(perm, F, slot(2), ss, Meth::c_rt(5, 4));
+            } else {
+                scatter_perm<n>(perm, F, slot(1), ss);   // K_5 (natural order) in the free slot
+#pragma unroll
+                for (int i = 0; i < n; ++i) ylast[i] = ys[i];
+            }
+        }
+    } else {
+        double Flast[Meth::reuse_last ? n : 1];   // f of the last new stage point (methods reusing it)
+        {   // stage 0: K_0 = A^{-1} f(y)
+            double x[n];
+#pragma unroll
+            for (int i = 0; i < n; ++i) x[i] = f0[i];
             if constexpr (Meth::reuse_last) {
 #pragma unroll
-                for (int i = 0; i < n; ++i) Flast[i] = F[i];
+                for (int i = 0; i < n; ++i) Flast[i] = f0[i];
             }
-        } else {
-            // the stage point equals the previous new one (a_sj = a_(s-1)j): reuse its f
-#pragma unroll
-            for (int i = 0; i < n; ++i) F[i] = Flast[i];
+            lu_solve<n>(A, x);
+            scatter_perm<n>(perm, x, slot(0), ss);
         }
+#pragma unroll 1
+        for (int s = 1; s < S; ++s) {
+            double F[n];
+            double ys[n];
 #pragma unroll
-        for (int j = 0; j < S - 1; ++j) {
-            if (j < s) {
-                const double c = Meth::c_rt(s, j) * hinv;
+            for (int i = 0; i < n; ++i) ys[i] = C.y[i];
+            if (!Meth::reuse_last || Meth::newf_rt(s)) {
 #pragma unroll
-                for (int i = 0; i < n; ++i) F[i] = fma(c, Ks[(j * n + i) * ss], F[i]);
+                for (int j = 0; j < S - 1; ++j) {
+                    if (j < s) {
+                        const double a = Meth::a_rt(s, j);
+#pragma unroll
+                        for (int i = 0; i < n; ++i) ys[i] = fma(a, slot(j)[i * ss], ys[i]);
+                    }
+                }
+                if constexpr (DAE) {
+                    double Ts = C.y[M::NSA];
+                    stage_ok = rhs_dae<M>(P, C.rho, invrho, C.e, ys, C.Yin, Ts, F) && stage_ok;
+                } else {
+                    rhs<M>(P, C.rho, invrho, ys, C.Yin, F);
+                }
+                cnt.rhs++;
+                if constexpr (Meth::reuse_last) {
+#pragma unroll
+                    for (int i = 0; i < n; ++i) Flast[i] = F[i];
+                }
+            } else {
+                // the stage point equals the previous new one (a_sj = a_(s-1)j): reuse its f
+#pragma unroll
+                for (int i = 0; i < n; ++i) F[i] = Flast[i];
             }
-        }
-        // the last stage of a stiffly accurate method solves in slot 0 (K_0 is no longer needed)
-        const bool last_stage = Meth::stiff_last && (s == S - 1);
-        double* v = Ks + ((last_stage ? 0 : s) * n) * ss;
 #pragma unroll
-        for (int i = 0; i < n; ++i) v[i * ss] = F[i];
-        double x[n];
-        lu_solve<n>(A, piv, v, ss, x);
-        if (last_stage) {
+            for (int j = 0; j < S - 1; ++j) {
+                if (j < s) {
+                    const double c = Meth::c_rt(s, j) * hinv;
 #pragma unroll
-            for (int i = 0; i < n; ++i) { ylast[i] = ys[i]; xlast[i] = x[i]; }
+                    for (int i = 0; i < n; ++i) F[i] = fma(c, slot(j)[i * ss], F[i]);
+                }
+            }
+            lu_solve<n>(A, F);
+            // the last stage of a stiffly accurate method goes to slot 0 (K_0 is no longer needed)
+            const bool last_stage = Meth::stiff_last && (s == S - 1);
+            scatter_perm<n>(perm, F, slot(last_stage ? 0 : s), ss);
+            if (last_stage) {
+#pragma unroll
+                for (int i = 0; i < n; ++i) ylast[i] = ys[i];
+            }
         }
     }
 
@@ -348,14 +430,15 @@ __device__ __forceinline__ int ros_step(const Params<M>& P, const LaunchCtx& L, 
     for (int i = 0; i < n; ++i) {
         double v, ev;
         if constexpr (Meth::stiff_last) {
-            v = ylast[i] + xlast[i];      // y + sum m_j K_j = Y_last + K_last
-            ev = xlast[i];                // sum e_j K_j = K_last
+            const double xl = slot(Meth::collapse ? 1 : 0)[i * ss];   // K_last
+            v = ylast[i] + xl;            // y + sum m_j K_j = Y_last + K_last
+            ev = xl;                      // sum e_j K_j = K_last
         } else {
             v = C.y[i];
             ev = 0.0;
             static_for<0, S>([&](auto j_) {
                 constexpr int j = decltype(j_)::value;
-                const double kj = Ks[(j * n + i) * ss];
+                const double kj = slot(j)[i * ss];
                 if constexpr (Meth::m(j) != 0.0) v = fma(Meth::m(j), kj, v);
                 if constexpr (Meth::e(j) != 0.0) ev = fma(Meth::e(j), kj, ev);
             });

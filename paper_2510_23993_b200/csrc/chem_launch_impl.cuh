@@ -26,7 +26,7 @@ cudaError_t Launch<M, Meth, DAE>::lock(const Params<M>& p, const LaunchCtx& L, c
 {
     // persistent: one block per SM walks tiles blockIdx.x, blockIdx.x + gridDim.x, ...
     constexpr size_t b = SmemLayout<M, Meth, DAE>::bytes_per_thread;
-    constexpr int BS = b == 0 ? 224 : (int)std::min<size_t>(224, (227 * 1024 / (b == 0 ? 1 : b)) / 32 * 32);
+    constexpr int BS = b == 0 ? 256 : (int)std::min<size_t>(256, (227 * 1024 / (b == 0 ? 1 : b)) / 32 * 32);
     constexpr size_t sm = b * BS;
     auto kern = k_integrate<M, Meth, BS, DAE, true>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
