@@ -83,7 +83,9 @@ typedef struct {
 typedef struct {
     double T_min;           /* gate T_reaction_min (value unstated -> 500 K) */
     int32_t kmax_bulk;      /* attempted substeps per cell per bulk launch (K_max = 5)     */
-    int64_t n_active_star;  /* bulk->sparse threshold N*_active (1e4)               */
+    int64_t n_active_star;  /* bulk->sparse threshold N*_active (the paper's 1e4 is
+                               H100-tuned).  < 0 (default): one resident wave of the integration
+                               kernel, SMs x resident cells per SM (37 888 on a B200)             */
     int32_t kmax_sparse;    /* attempted substeps in the sparse launch (1e5)              */
     double atol_T;          /* absolute tolerance on the integrated temperature, K               */
     int32_t method;         /* CHEM_METHOD_*                                                      */

@@ -334,7 +334,7 @@ int validate(const chem_mech_desc* d)
 
 // ------------------------------------------------------------------ workspace layout
 struct WsLayout {
-    size_t stats, boxes, start, cell_t, cell_h, steps, state, ids0, idsA, idsB, total;
+    size_t stats, boxes, start, cell_t, cell_h, steps, box, state, ids0, idsA, idsB, total;
 };
 
 inline size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -349,6 +349,7 @@ WsLayout ws_layout(int64_t N, int32_t B)
     w.cell_t = o; o = al256(o + (size_t)N * 8);
     w.cell_h = o; o = al256(o + (size_t)N * 8);
     w.steps = o; o = al256(o + (size_t)N * 4);
+    w.box = o; o = al256(o + (size_t)N * 4);
     w.state = o; o = al256(o + (size_t)N);
     w.ids0 = o; o = al256(o + (size_t)N * 4);
     w.idsA = o; o = al256(o + (size_t)N * 4);
@@ -419,7 +420,7 @@ void chem_default_opts(chem_opts* o)
     if (!o) return;
     o->T_min = 500.0;
     o->kmax_bulk = 5;
-    o->n_active_star = 10000;
+    o->n_active_star = -1;      // auto: one resident wave of the integration kernel (37 888 on B200)
     o->kmax_sparse = 100000;
     o->atol_T = 1e-6;
     o->method = CHEM_METHOD_RODAS4;
@@ -448,7 +449,7 @@ const char* chem_strerror(int code)
 
 static int check_opts(const chem_opts* o)
 {
-    if (o->kmax_bulk < 1 || o->kmax_sparse < 1 || o->n_active_star < 0 || !(o->atol_T > 0.0) ||
+    if (o->kmax_bulk < 1 || o->kmax_sparse < 1 || !(o->atol_T > 0.0) ||
         (o->method < CHEM_METHOD_RODAS4 || o->method > CHEM_METHOD_ROS4) ||
         !std::isfinite(o->T_min) || !(o->eps_change > 0.0 && o->eps_change <= 1.0) ||
         (o->temperature_mode != 0 && o->temperature_mode != 1) || (o->refill_bulk != 0 && o->refill_bulk != 1) ||
@@ -648,6 +649,7 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
     L.cell_h = reinterpret_cast<double*>(base + W.cell_h);
     L.state = reinterpret_cast<uint8_t*>(base + W.state);
     L.cell_steps = reinterpret_cast<int32_t*>(base + W.steps);
+    L.cell_box = reinterpret_cast<int32_t*>(base + W.box);
     L.stats = reinterpret_cast<unsigned long long*>(base + W.stats);
     L.rtol = rtol;
     L.atol = atol;
@@ -716,7 +718,15 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
                       (o.lockstep == 1 || (o.lockstep == 2 && c->simt_eff < kLockEff));
     st.lockstep = lock;
     unsigned long long att_skip = 0, ws_skip = 0;   // the one-substep first burst is not a SIMT sample
-    while (n_cur > o.n_active_star && n_cur > 0) {
+    // N* (P:181): negative = one resident wave of the integration kernel (SMs x resident cells per SM):
+    // below it a bulk burst can no longer fill the GPU, so the persistent sparse launch takes over
+    // (B200 sweep, profiles/r01_nstar_sweep.txt; the paper's 1e4 was tuned on H100).
+    const int64_t nstar = o.n_active_star >= 0 ? o.n_active_star
+                          : use_grp ? (int64_t)c->num_sms * ops.grp_blocks_per_sm(o.method, o.lanes_per_cell) *
+                                          (kGrpBS / o.lanes_per_cell)
+                                    : (int64_t)c->num_sms * ops.blocks_per_sm(o.method, o.temperature_mode) *
+                                          kIntegrateBS;
+    while (n_cur > nstar && n_cur > 0) {
         const bool first_burst = lock && st.bulk_iters == 0 && o.kmax_first > 0;
         const int kmax_b = first_burst ? o.kmax_first : o.kmax_bulk;
         const bool all_cells = !o.compact_bulk;

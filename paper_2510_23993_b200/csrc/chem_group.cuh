@@ -691,7 +691,7 @@ __device__ __forceinline__ bool g_load(const GTable<M>& tb, const Grp<G>& gr, co
     using LY = GLayout<M>;
     using O = GOwn<M, G>;
     C.g = g;
-    C.b = find_box(L, g);
+    C.b = L.cell_box[g];
     const DevBox bx = L.boxes[C.b];
     C.off = g - L.box_start[C.b];
     C.ld = bx.ld;

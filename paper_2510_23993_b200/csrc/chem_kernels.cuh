@@ -49,6 +49,8 @@ struct LaunchCtx {
     double* cell_h;            // [total] next substep size
     uint8_t* state;            // [total] CellState (+ bit 7: last step rejected)
     int32_t* cell_steps;       // [total] attempted substeps summed over launches
+    int32_t* cell_box;         // [total] box of each active cell (written by the gate: one coalesced
+                               // load in load_cell instead of a dependent-load binary search)
     unsigned long long* stats; // [S_NSTATS]
     double rtol, atol, atolT, T_min;
     double eps_change;          // explicit scheme: max fractional change per step
@@ -111,7 +113,7 @@ __global__ void __launch_bounds__(BS) k_gate(LaunchCtx L, uint32_t* ids_out)
             const double T = bx.T[off];
             act = (T >= L.T_min) && !(bx.solid && bx.solid[off]);   // Alg. 3 §1
             L.state[g] = act ? ST_FRESH : ST_INACTIVE;
-            if (act) L.cell_steps[g] = 0;
+            if (act) { L.cell_steps[g] = 0; L.cell_box[g] = b; }
         }
         block_compact<BS>(act, (uint32_t)g, ids_out, &L.stats[S_COUNT_ACTIVE]);
     }
@@ -517,7 +519,7 @@ __device__ __forceinline__ void load_cell(const Params<M>& P, const LaunchCtx& L
                                           uint8_t st, Counters& cnt, bool& ok)
 {
     C.g = g;
-    C.b = find_box(L, g);
+    C.b = L.cell_box[g];
     const DevBox bx = L.boxes[C.b];
     C.off = g - L.box_start[C.b];
     C.ld = bx.ld;

@@ -44,7 +44,8 @@ def test_library_is_sm100a_only():
 def test_default_opts_are_the_papers():
     from paper_2510_23993_b200 import binding
     o = binding.default_opts()
-    assert (o.kmax_bulk, o.n_active_star, o.kmax_sparse, o.T_min) == (5, 10000, 100000, 500.0)
+    # P:179 K_max = 5, P:181 N* (default < 0: one resident wave of the integration kernel)
+    assert (o.kmax_bulk, o.n_active_star, o.kmax_sparse, o.T_min) == (5, -1, 100000, 500.0)
     assert (o.lockstep, o.kmax_first, o.refill_bulk, o.compact_bulk) == (2, 1, 0, 1)
 
 
