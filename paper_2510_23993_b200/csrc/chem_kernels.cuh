@@ -614,6 +614,7 @@ __global__ void __launch_bounds__(BS) k_integrate(const __grid_constant__ Params
                                                   int refill, int final_phase)
 {
     extern __shared__ double smem[];
+    fm_tables_to_smem();
     using SL = SmemLayout<M, Meth, DAE>;
     constexpr int n = SL::n;
     double* mine = smem + threadIdx.x;
@@ -687,6 +688,7 @@ __global__ void __launch_bounds__(128, MINB) k_rates(const __grid_constant__ Par
                                                     const double* __restrict__ rho,
                         const double* __restrict__ T, const double* __restrict__ Y, double* __restrict__ wdot)
 {
+    fm_tables_to_smem();
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         double Yc[M::NS];
 #pragma unroll
@@ -704,6 +706,7 @@ template <class M>
 __global__ void k_rhs(const __grid_constant__ Params<M> P, int64_t n, int64_t ld, const double* __restrict__ rho,
                       const double* __restrict__ T, const double* __restrict__ Y, double* __restrict__ f)
 {
+    fm_tables_to_smem();
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         double Yc[M::NS], y[M::NSA + 1], fo[M::NSA + 1];
 #pragma unroll
@@ -725,6 +728,7 @@ __global__ void __launch_bounds__(BS) k_jacobian(const __grid_constant__ Params<
                                                  const double* __restrict__ Y, double* __restrict__ J)
 {
     extern __shared__ double smem[];
+    fm_tables_to_smem();
     constexpr int nn = M::NS + 1;
     SMat A{smem + threadIdx.x, BS, nn};
     const int64_t i = (int64_t)blockIdx.x * BS + threadIdx.x;
