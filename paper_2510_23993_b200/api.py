@@ -221,16 +221,9 @@ class HostRunner:
 
     def __init__(self, chem: Chem, host_boxes, calls=None, chunks=4):
         self.chem = chem
-        self.host = host_boxes          # list of dict(rho, e, T, Y, dt) pinned CPU tensors
         self.calls = calls or [list(range(len(host_boxes)))]
         dev = chem.device
-        self.dev_boxes = [Box(torch.empty_like(h["rho"], device=dev), torch.empty_like(h["e"], device=dev),
-                              torch.empty_like(h["T"], device=dev), torch.empty_like(h["Y"], device=dev), h["dt"])
-                          for h in host_boxes]
-        self.out_T = [torch.empty_like(h["T"]).pin_memory() for h in host_boxes]
-        self.out_Y = [torch.empty_like(h["Y"]).pin_memory() for h in host_boxes]
-        self.h2d_bytes = sum(sum(h[k].numel() * 8 for k in ("rho", "e", "T", "Y")) for h in host_boxes)
-        self.d2h_bytes = sum(h["T"].numel() * 8 + h["Y"].numel() * 8 for h in host_boxes)
+        nb = len(host_boxes)
         self.pipelined = len(self.calls) == 1 and len(self.calls[0]) >= chunks > 1
         if self.pipelined:
             ids = self.calls[0]
@@ -238,37 +231,63 @@ class HostRunner:
             self.groups = [ids[i:i + k] for i in range(0, len(ids), k)]
             self.s_h2d = torch.cuda.Stream(dev)
             self.s_d2h = torch.cuda.Stream(dev)
+        else:
+            self.groups = [list(range(nb))]
+        # One pinned input slab, one pinned output slab and one device slab per group, laid out as
+        # [rho_*][e_*][T_*][Y_*] (component-major boxes back to back): a step moves each group with ONE
+        # H2D copy of the slab and ONE D2H copy of its [T_*][Y_*] tail, instead of 4 + 2 copies per box.
+        self.dev_boxes = [None] * nb
+        self.out_T, self.out_Y = [None] * nb, [None] * nb
+        self.slabs = []
+        for grp in self.groups:
+            n = [host_boxes[i]["rho"].numel() for i in grp]
+            ns = [host_boxes[i]["Y"].shape[0] for i in grp]
+            tot = sum(n)
+            size = 3 * tot + sum(a * c for a, c in zip(n, ns))
+            h_in = torch.empty(size, dtype=torch.float64).pin_memory()
+            h_out = torch.empty(size - 2 * tot, dtype=torch.float64).pin_memory()
+            d = torch.empty(size, dtype=torch.float64, device=dev)
+            o = [0, tot, 2 * tot, 3 * tot]   # rho, e, T, Y cursors
+            for i, ni, si in zip(grp, n, ns):
+                h = host_boxes[i]
+                h_in[o[0]:o[0] + ni].copy_(h["rho"].reshape(-1))
+                h_in[o[1]:o[1] + ni].copy_(h["e"].reshape(-1))
+                h_in[o[2]:o[2] + ni].copy_(h["T"].reshape(-1))
+                h_in[o[3]:o[3] + ni * si].copy_(h["Y"].reshape(-1))
+                self.dev_boxes[i] = Box(d[o[0]:o[0] + ni], d[o[1]:o[1] + ni], d[o[2]:o[2] + ni],
+                                        d[o[3]:o[3] + ni * si].view(si, ni), h["dt"])
+                self.out_T[i] = h_out[o[2] - 2 * tot:o[2] - 2 * tot + ni]
+                self.out_Y[i] = h_out[o[3] - 2 * tot:o[3] - 2 * tot + ni * si].view(si, ni)
+                o = [o[0] + ni, o[1] + ni, o[2] + ni, o[3] + ni * si]
+            self.slabs.append((h_in, h_out, d, 2 * tot))
+        self.h2d_bytes = sum(s_[0].numel() * 8 for s_ in self.slabs)
+        self.d2h_bytes = sum(s_[1].numel() * 8 for s_ in self.slabs)
 
-    def _h2d(self, idx):
-        for i in idx:
-            h, d = self.host[i], self.dev_boxes[i]
-            d.rho.copy_(h["rho"], non_blocking=True)
-            d.e.copy_(h["e"], non_blocking=True)
-            d.T.copy_(h["T"], non_blocking=True)
-            d.Y.copy_(h["Y"], non_blocking=True)
+    def _h2d_group(self, g):
+        h_in, _, d, _ = self.slabs[g]
+        d.copy_(h_in, non_blocking=True)
 
-    def _d2h(self, idx):
-        for i in idx:
-            self.out_T[i].copy_(self.dev_boxes[i].T, non_blocking=True)
-            self.out_Y[i].copy_(self.dev_boxes[i].Y, non_blocking=True)
+    def _d2h_group(self, g):
+        _, h_out, d, t0 = self.slabs[g]
+        h_out.copy_(d[t0:], non_blocking=True)
 
     def step(self, rtol, atol):
         if not self.pipelined:
-            self._h2d(range(len(self.host)))
+            self._h2d_group(0)
             st = [self.chem.integrate_boxes([self.dev_boxes[i] for i in c], rtol=rtol, atol=atol) for c in self.calls]
-            self._d2h(range(len(self.host)))
+            self._d2h_group(0)
             return st
         comp = torch.cuda.current_stream(self.chem.device)
         ev_in = [torch.cuda.Event() for _ in self.groups]
         st = []
         with torch.cuda.stream(self.s_h2d):
             self.s_h2d.wait_stream(comp)            # the previous step's D2H reads must not be overwritten early
-            self._h2d(self.groups[0])
+            self._h2d_group(0)
             ev_in[0].record(self.s_h2d)
         for g, idx in enumerate(self.groups):
             if g + 1 < len(self.groups):
                 with torch.cuda.stream(self.s_h2d):
-                    self._h2d(self.groups[g + 1])
+                    self._h2d_group(g + 1)
                     ev_in[g + 1].record(self.s_h2d)
             comp.wait_event(ev_in[g])
             st.append(self.chem.integrate_boxes([self.dev_boxes[i] for i in idx], rtol=rtol, atol=atol))
@@ -276,7 +295,7 @@ class HostRunner:
             done.record(comp)
             with torch.cuda.stream(self.s_d2h):
                 self.s_d2h.wait_event(done)
-                self._d2h(idx)
+                self._d2h_group(g)
         comp.wait_stream(self.s_d2h)                # the step ends when the last result is on the host
         return st
 

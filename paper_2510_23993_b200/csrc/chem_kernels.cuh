@@ -458,7 +458,9 @@ __device__ __forceinline__ int ros_step(const Params<M>& P, const LaunchCtx& L, 
         return 0;
     }
     // step-size controller (Hairer-Wanner IV.8; KPP Rosenbrock): safety 0.9, factor in [0.2, 6]
-    double fac = 0.9 * pow(err, -Meth::err_exp);
+    double fac;
+    if constexpr (Meth::err_exp == 0.25) fac = 0.9 / sqrt(sqrt(err));   // err^(-1/4) without libdevice pow
+    else fac = 0.9 * pow(err, -Meth::err_exp);
     fac = fmin(6.0, fmax(0.2, fac));
     double hnew = h * fac;
     if (err <= 1.0) {
@@ -627,38 +629,8 @@ __global__ void __launch_bounds__(BS) k_integrate(const __grid_constant__ Params
     bool live = true;     // this thread may still take a cell
     bool first = true;
     int64_t tile = blockIdx.x;
-    for (;;) {
-        while (!have && live) {
-            int64_t idx;
-            if (refill) {
-                idx = (int64_t)atomicAdd(&L.stats[S_CURSOR], 1ull);
-            } else if (LOCK) {
-                idx = first ? tile * BS + threadIdx.x : n_ids;   // persistent: tiles blockIdx.x + k*gridDim.x
-                first = false;
-            } else {
-                idx = first ? (int64_t)blockIdx.x * BS + threadIdx.x : n_ids;
-                first = false;
-            }
-            if (idx >= n_ids) { live = false; break; }
-            const uint32_t g = ids ? ids[idx] : (uint32_t)idx;
-            const uint8_t st = L.state[g];
-            if ((st & 0x7f) != ST_FRESH && (st & 0x7f) != ST_RUNNING) continue;
-            bool ok;
-            load_cell<M>(P, L, g, C, st, cnt, ok);
-            if (!ok) { L.state[g] = ST_FAILED; continue; }
-            have = true;
-        }
-        if constexpr (LOCK) {
-            if (!__syncthreads_or(have)) {
-                if (refill) break;
-                tile += gridDim.x;                  // block-uniform: next tile of this persistent block
-                if (tile * BS >= n_ids) break;
-                first = true;
-                live = true;
-                continue;
-            }
-            if (!have) continue;
-        } else if (!have) break;
+    // one attempted substep of the lane's cell and its write-back when the cell leaves the launch
+    auto substep = [&]() {
         {   // SIMT efficiency statistic: the lowest lane executing this substep counts one warp substep
             const unsigned am = __activemask();
             if ((int)(threadIdx.x & 31) == __ffs(am) - 1) cnt.warp_substeps++;
@@ -677,6 +649,63 @@ __global__ void __launch_bounds__(BS) k_integrate(const __grid_constant__ Params
             store_cell<M>(P, L, C, final_phase ? ST_UNFINISHED : ST_RUNNING, cnt);
             have = false;
         }
+    };
+    // take list entry idx (if it is still an active cell): load its state
+    auto take = [&](int64_t idx) {
+        const uint32_t g = ids ? ids[idx] : (uint32_t)idx;
+        const uint8_t st = L.state[g];
+        if ((st & 0x7f) != ST_FRESH && (st & 0x7f) != ST_RUNNING) return;
+        bool ok;
+        load_cell<M>(P, L, g, C, st, cnt, ok);
+        if (!ok) { L.state[g] = ST_FAILED; return; }
+        have = true;
+    };
+    constexpr unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    for (;;) {
+        if (!LOCK && refill) {
+            // Persistent lane refill, batched per warp: idle lanes wait until a quarter of the warp
+            // is idle (or nothing runs), then take consecutive list entries with one warp-aggregated
+            // atomic and load them together, so the dependent-load latency of a cell load is paid
+            // once per batch instead of once per finished lane.  All 32 lanes stay in the loop until
+            // the warp's work is exhausted (the ballots name the full warp).
+            for (;;) {
+                const unsigned need = __ballot_sync(FULL, !have && live);
+                if (need == 0) break;
+                const unsigned busy = __ballot_sync(FULL, have);
+                if (busy != 0 && __popc(need) < 8) break;
+                const int leader = __ffs(need) - 1;
+                unsigned long long base = 0;
+                if (lane == leader) base = atomicAdd(&L.stats[S_CURSOR], (unsigned long long)__popc(need));
+                base = __shfl_sync(FULL, base, leader);
+                if (!have && live) {
+                    const int64_t idx = (int64_t)base + __popc(need & ((1u << lane) - 1u));
+                    if (idx >= n_ids) live = false;
+                    else take(idx);
+                }
+            }
+            if (!__any_sync(FULL, have)) break;
+            if (!have) continue;
+        } else {
+            while (!have && live) {
+                const int64_t idx = !first ? n_ids : LOCK ? tile * BS + threadIdx.x   // persistent tiles
+                                                          : (int64_t)blockIdx.x * BS + threadIdx.x;
+                first = false;
+                if (idx >= n_ids) { live = false; break; }
+                take(idx);
+            }
+            if constexpr (LOCK) {
+                if (!__syncthreads_or(have)) {
+                    tile += gridDim.x;                  // block-uniform: next tile of this persistent block
+                    if (tile * BS >= n_ids) break;
+                    first = true;
+                    live = true;
+                    continue;
+                }
+                if (!have) continue;
+            } else if (!have) break;
+        }
+        substep();
     }
     __syncwarp();   // all lanes of the warp reach here (no early returns): reconverge for the reduction
     flush_counters(L, cnt);

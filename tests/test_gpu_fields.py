@@ -222,3 +222,32 @@ def test_activity_trace_app_b(ora, doc):
     lines = activity_lines(tr, boxes, t=1e-7, kmax=5)
     assert lines[0].startswith("Level 0, FAB 0, t = 1e-07, step = 0, n_cells = 262144, n_active = ")
     ch.set_trace(0, 0)
+
+
+@pytest.mark.parametrize("chunks", [1, 3])
+def test_host_runner_matches_device_path(chem, doc, chunks):
+    """The e2e path (HostRunner: pinned slabs, one H2D and one D2H copy per group, copy/compute
+    pipelining) returns bitwise the same (T, Y) as the device-resident call on the same boxes."""
+    from paper_2510_23993_b200.api import HostRunner
+    rng = np.random.default_rng(5)
+    d = synth.cfg1b(doc, n=6 * 512)
+    host, dev_boxes = [], []
+    for b in range(6):
+        sl = slice(b * 512, (b + 1) * 512)
+        T = torch.tensor(d["T"][sl], dtype=torch.float64)
+        Y = torch.tensor(d["Y"][sl].T.copy(), dtype=torch.float64)
+        rho = torch.tensor(d["rho"][sl], dtype=torch.float64)
+        e = chem.energy(T.to(DEV), Y.to(DEV)).cpu()
+        host.append(dict(rho=rho.pin_memory(), e=e.pin_memory(), T=T.pin_memory(), Y=Y.pin_memory(), dt=d["dt"]))
+        dev_boxes.append(Box(rho.to(DEV), e.to(DEV), T.to(DEV), Y.to(DEV), d["dt"]))
+    chem.integrate_boxes(dev_boxes, **GPU_TOL)
+    hr = HostRunner(chem, host, chunks=chunks)
+    assert hr.pipelined == (chunks > 1)
+    for _ in range(2):                                   # a second step starts from the same inputs
+        hr.step(**GPU_TOL)
+        torch.cuda.synchronize()
+        for i, b in enumerate(dev_boxes):
+            assert torch.equal(hr.out_T[i], b.T.cpu()) and torch.equal(hr.out_Y[i], b.Y.cpu())
+    assert hr.h2d_bytes == 6 * 512 * (3 + len(doc["species"])) * 8
+    assert hr.d2h_bytes == 6 * 512 * (1 + len(doc["species"])) * 8
+    del rng
