@@ -223,7 +223,7 @@ __device__ __forceinline__ int ros_step(const Params<M>& P, const LaunchCtx& L, 
 {
     constexpr int n = DAE ? M::NSA : M::NSA + 1;
     constexpr int S = Meth::S;
-    const double invrho = 1.0 / C.rho;
+    const double invrho = frcp(C.rho);
     double f0[n];
     if constexpr (DAE) {
         double Yf[M::NS];
@@ -447,9 +447,10 @@ __device__ __forceinline__ int ros_step(const Params<M>& P, const LaunchCtx& L, 
         }
         ynew[i] = v;
         const double s = ((i < M::NSA) ? L.atol : L.atolT) + L.rtol * fmax(fabs(C.y[i]), fabs(v));
-        err = fma(ev / s, ev / s, err);
+        const double q = ev * frcp(s);
+        err = fma(q, q, err);
     }
-    err = sqrt(err / n);
+    err = sqrt(err * (1.0 / n));
     cnt.attempted++;
     C.k++;
     if (!ok || !stage_ok || !isfinite(err)) {  // singular matrix or non-finite stage: shrink hard, retry
