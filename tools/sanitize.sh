@@ -12,8 +12,8 @@ m = load_mechanism("h2air_li2004")
 d = synth.cfg1c(m.species, m.W)
 idx = np.arange(0, 4096, 64)
 dev = torch.device("cuda", 0)
-for lanes in (1, 8):
-    ch = Chem("h2air_li2004", device=0, lanes_per_cell=lanes, kmax_bulk=3, n_active_star=16)
+for lanes, lock in ((1, 0), (8, 0), (1, 1)):
+    ch = Chem("h2air_li2004", device=0, lanes_per_cell=lanes, kmax_bulk=3, n_active_star=16, lockstep=lock)
     T = torch.tensor(d["T"][idx], device=dev)
     Y = torch.tensor(d["Y"][idx].T.copy(), device=dev)
     rho = torch.tensor(d["rho"][idx], device=dev)
@@ -26,7 +26,7 @@ for lanes in (1, 8):
     w = ch.rates(rho, T, Y)
     J = ch.jacobian(rho[:8], T[:8], Y[:, :8].contiguous())
     torch.cuda.synchronize()
-    print("lanes", lanes, st["steps_attempted"], st["sparse_cells"])
+    print("lanes", lanes, "lockstep", lock, st["steps_attempted"], st["sparse_cells"])
 PY
 for tool in memcheck racecheck synccheck initcheck; do
   timeout 900 compute-sanitizer --tool $tool --print-limit 20 python /tmp/san_case.py > gpurun_out/sanitize_$tool.txt 2>&1
