@@ -462,7 +462,9 @@ def ours(args):
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches, "clocks": clk,
             "detail": {"step_ms": step_ms, "rank0_seconds": t_rank, "k_integrate_ms": k_ms / args.steps,
                        "integrate_launches": launches_int, "substeps_per_cell_step": att / max(wl.cell_steps, 1),
-                       "accepted_per_cell_step": acc / max(wl.cell_steps, 1), "bulk_iters": s0["bulk_iters"],
+                       "accepted_per_cell_step": acc / max(wl.cell_steps, 1),
+                       "frozen_per_cell_step": sum(s.get("steps_frozen", 0) for s in stats) / args.steps
+                       / max(wl.cell_steps, 1), "bulk_iters": s0["bulk_iters"],
                        "active_per_iter": s0["active_per_iter"], "sparse_cells": s0["sparse_cells"],
                        "active0": s0["active0"], "t_gate_ms": s0["t_gate_ms"], "t_compact_ms": s0["t_compact_ms"],
                        "t_sparse_ms": s0["t_sparse_ms"], "n_unfinished": s0["n_unfinished"],

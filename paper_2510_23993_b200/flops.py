@@ -55,9 +55,12 @@ class FlopModel:
 
     def flops(self, stats):
         """Algorithmic FLOPs of one chem_integrate call from its chem_stats counters."""
-        att = stats["steps_attempted"] - stats.get("steps_frozen", 0)   # frozen steps: RHS + J, no LU/solves
-        return (stats["rhs_evals"] * self.rhs + stats["jac_evals"] * self.jac + stats["lu_count"] * self.lu
-                + att * (self.stages * self.solve + self.control))
+        frozen = stats.get("steps_frozen", 0)
+        att = stats["steps_attempted"] - frozen   # frozen steps: one RHS (y += dt f), no LU/solves
+        # a frozen step evaluates J in the kernel (rhs_jac runs before the frozen test) but the method
+        # needs only f there, so J is not charged for it: algorithmic work, not executed work
+        return (stats["rhs_evals"] * self.rhs + (stats["jac_evals"] - frozen) * self.jac
+                + stats["lu_count"] * self.lu + att * (self.stages * self.solve + self.control))
 
     def per_step(self):
         return self.stages * self.rhs + self.jac + self.lu + self.stages * self.solve + self.control
