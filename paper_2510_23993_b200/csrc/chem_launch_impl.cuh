@@ -8,13 +8,27 @@
 
 namespace chem {
 
+// cudaFuncSetAttribute / occupancy queries are host API calls of ~10 us each: do them once per kernel
+// and device (one process drives one GPU; the cache key is the current device) instead of per launch.
+template <class K>
+inline cudaError_t set_smem_once(K kern, size_t bytes)
+{
+    static int done_dev = -1;
+    int d = 0;
+    cudaGetDevice(&d);
+    if (d == done_dev) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) done_dev = d;
+    return e;
+}
+
 template <class M, class Meth, bool DAE>
 cudaError_t Launch<M, Meth, DAE>::run(const Params<M>& p, const LaunchCtx& L, const uint32_t* ids, int64_t n,
                                       int kmax, int refill, int fin, int grid, cudaStream_t s)
 {
     auto kern = k_integrate<M, Meth, kIntegrateBS, DAE>;
     cudaError_t e = cudaSuccess;
-    if (smem() > 0) e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem());
+    if (smem() > 0) e = set_smem_once(kern, smem());
     if (e != cudaSuccess) return e;
     kern<<<grid, kIntegrateBS, smem(), s>>>(p, L, ids, n, kmax, refill, fin);
     return cudaGetLastError();
@@ -29,7 +43,7 @@ cudaError_t Launch<M, Meth, DAE>::lock(const Params<M>& p, const LaunchCtx& L, c
     constexpr int BS = b == 0 ? 256 : (int)std::min<size_t>(256, (227 * 1024 / (b == 0 ? 1 : b)) / 32 * 32);
     constexpr size_t sm = b * BS;
     auto kern = k_integrate<M, Meth, BS, DAE, true>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaError_t e = set_smem_once(kern, sm);
     if (e != cudaSuccess) return e;
     const int grid = (int)std::min<int64_t>((n + BS - 1) / BS, nsm);
     kern<<<grid, BS, sm, s>>>(p, L, ids, n, kmax, 0, fin);
@@ -39,10 +53,16 @@ cudaError_t Launch<M, Meth, DAE>::lock(const Params<M>& p, const LaunchCtx& L, c
 template <class M, class Meth, bool DAE>
 int Launch<M, Meth, DAE>::blocks_per_sm()
 {
-    int nb = 0;
-    auto kern = k_integrate<M, Meth, kIntegrateBS, DAE>;
-    if (smem() > 0) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem());
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kIntegrateBS, smem());
+    static int dev = -1, nb = 0;
+    int d = 0;
+    cudaGetDevice(&d);
+    if (d != dev) {
+        auto kern = k_integrate<M, Meth, kIntegrateBS, DAE>;
+        if (smem() > 0) set_smem_once(kern, smem());
+        nb = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kIntegrateBS, smem());
+        dev = d;
+    }
     return std::max(nb, 1);
 }
 
