@@ -9,11 +9,12 @@
 namespace chem {
 
 // cudaFuncSetAttribute / occupancy queries are host API calls of ~10 us each: do them once per kernel
-// and device (one process drives one GPU; the cache key is the current device) instead of per launch.
+// and device (one process drives one GPU) instead of per launch.  `done_dev` must be a static of the
+// caller's own instantiation (one per kernel): a static keyed on the kernel's function-pointer TYPE
+// would be shared by every k_integrate variant with the same signature.
 template <class K>
-inline cudaError_t set_smem_once(K kern, size_t bytes)
+inline cudaError_t set_smem_once(int& done_dev, K kern, size_t bytes)
 {
-    static int done_dev = -1;
     int d = 0;
     cudaGetDevice(&d);
     if (d == done_dev) return cudaSuccess;
@@ -28,7 +29,8 @@ cudaError_t Launch<M, Meth, DAE>::run(const Params<M>& p, const LaunchCtx& L, co
 {
     auto kern = k_integrate<M, Meth, kIntegrateBS, DAE>;
     cudaError_t e = cudaSuccess;
-    if (smem() > 0) e = set_smem_once(kern, smem());
+    static int done_dev = -1;   // this instantiation's kernel
+    if (smem() > 0) e = set_smem_once(done_dev, kern, smem());
     if (e != cudaSuccess) return e;
     kern<<<grid, kIntegrateBS, smem(), s>>>(p, L, ids, n, kmax, refill, fin);
     return cudaGetLastError();
@@ -43,7 +45,8 @@ cudaError_t Launch<M, Meth, DAE>::lock(const Params<M>& p, const LaunchCtx& L, c
     constexpr int BS = b == 0 ? 256 : (int)std::min<size_t>(256, (227 * 1024 / (b == 0 ? 1 : b)) / 32 * 32);
     constexpr size_t sm = b * BS;
     auto kern = k_integrate<M, Meth, BS, DAE, true>;
-    cudaError_t e = set_smem_once(kern, sm);
+    static int done_dev = -1;   // this instantiation's (lockstep) kernel
+    cudaError_t e = set_smem_once(done_dev, kern, sm);
     if (e != cudaSuccess) return e;
     const int grid = (int)std::min<int64_t>((n + BS - 1) / BS, nsm);
     kern<<<grid, BS, sm, s>>>(p, L, ids, n, kmax, 0, fin);
@@ -58,7 +61,7 @@ int Launch<M, Meth, DAE>::blocks_per_sm()
     cudaGetDevice(&d);
     if (d != dev) {
         auto kern = k_integrate<M, Meth, kIntegrateBS, DAE>;
-        if (smem() > 0) set_smem_once(kern, smem());
+        if (smem() > 0) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem());
         nb = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kIntegrateBS, smem());
         dev = d;
