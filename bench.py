@@ -405,7 +405,7 @@ def ours(args):
                      Y=p[1].cpu().pin_memory(), dt=b.dt) for b, p in zip(wl.boxes, wl.pristine)]
         # copy/compute pipelining pays on dense fields; on sparse ones (cfg3/cfg4) splitting the fused
         # call serialises the chunks' long tails, so those run as one call
-        chunks = args.e2e_chunks if args.e2e_chunks > 0 else (4 if args.config in ("cfg2", "cfg5") else 1)
+        chunks = args.e2e_chunks if args.e2e_chunks > 0 else (5 if args.config in ("cfg2", "cfg5") else 1)
         hr = HostRunner(chem, host, wl.calls, chunks=chunks)
         hr.step(args.rtol, args.atol)
         torch.cuda.synchronize()

@@ -9,6 +9,7 @@ from __future__ import annotations
 import ctypes
 import dataclasses
 
+import numpy as np
 import torch
 
 from . import binding as _b
@@ -226,9 +227,12 @@ class HostRunner:
         nb = len(host_boxes)
         self.pipelined = len(self.calls) == 1 and len(self.calls[0]) >= chunks > 1
         if self.pipelined:
+            # tapered groups: the first group's H2D and the last group's D2H are the copies nothing
+            # overlaps, so those two groups get half the share of the middle ones
             ids = self.calls[0]
-            k = (len(ids) + chunks - 1) // chunks
-            self.groups = [ids[i:i + k] for i in range(0, len(ids), k)]
+            w = [1.0] + [2.0] * (chunks - 2) + [1.0] if chunks > 2 else [1.0] * chunks
+            cuts = np.round(np.cumsum([0.0] + w) / sum(w) * len(ids)).astype(int)
+            self.groups = [ids[cuts[g]:cuts[g + 1]] for g in range(chunks) if cuts[g + 1] > cuts[g]]
             self.s_h2d = torch.cuda.Stream(dev)
             self.s_d2h = torch.cuda.Stream(dev)
         else:
