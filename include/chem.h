@@ -101,7 +101,7 @@ typedef struct {
                                cell ends its burst early takes the next id); 0: one thread per id */
     double h0_factor;       /* first substep of a cell = h0_factor * |y|/|f(y)| (WRMS norms), capped
                                at dt (Hairer-Norsett-Wanner I.II.4 use 0.01)                      */
-    int32_t lockstep;       /* bulk bursts run as 224-thread blocks whose warps take every substep
+    int32_t lockstep;       /* bulk bursts run as 256-thread blocks whose warps take every substep
                                together (one barrier per substep), keeping an SM's warps in the same
                                code on heterogeneous fields (shared instruction cache):
                                0 off, 1 on, 2 auto (on while the previous call's bulk SIMT efficiency
@@ -109,11 +109,14 @@ typedef struct {
                                bitwise independent of this choice.                                */
     int32_t kmax_first;     /* substeps of the first bulk burst of a lockstep call (1: cells that
                                finish in one substep leave before the lockstep bursts); 0: kmax_bulk */
+    int32_t lockstep_sparse; /* the sparse launch as persistent 256-thread blocks with one barrier per
+                               substep and warp-batched lane refill (the lockstep of the bulk bursts
+                               applied to the tail): 0 off, 1 on.  Bitwise-neutral.               */
 } chem_opts;
 
 /* fills the paper's defaults: 500 K, 5, 1e4, 1e5, 1e-6 K, RODAS4, compact_bulk = 1, lanes_per_cell = 1,
    eps_change = 0.01, temperature_mode = 0,
-   refill_bulk = 0, h0_factor = 0.01, lockstep = 2 (auto), kmax_first = 1 */
+   refill_bulk = 0, h0_factor = 0.01, lockstep = 2 (auto), kmax_first = 1, lockstep_sparse = 0 */
 void chem_default_opts(chem_opts* o);
 
 /* ---- one AMR box / grid (FAB analogue) for the fused multi-box call ----------------- */

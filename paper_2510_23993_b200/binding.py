@@ -46,7 +46,7 @@ class ChemOpts(ctypes.Structure):
                 ("compact_bulk", ctypes.c_int32), ("lanes_per_cell", ctypes.c_int32),
                 ("eps_change", ctypes.c_double), ("temperature_mode", ctypes.c_int32),
                 ("refill_bulk", ctypes.c_int32), ("h0_factor", ctypes.c_double), ("lockstep", ctypes.c_int32),
-                ("kmax_first", ctypes.c_int32)]
+                ("kmax_first", ctypes.c_int32), ("lockstep_sparse", ctypes.c_int32)]
 
 
 class ChemBox(ctypes.Structure):

@@ -41,7 +41,7 @@ struct Ops {
     cudaError_t (*integrate)(const void*, int method, int dae, const LaunchCtx&, const uint32_t*, int64_t, int, int,
                              int, int grid, cudaStream_t);
     cudaError_t (*integrate_lock)(const void*, int method, int dae, const LaunchCtx&, const uint32_t*, int64_t,
-                                  int kmax, int fin, int nsm, cudaStream_t);
+                                  int kmax, int refill, int fin, int nsm, cudaStream_t);
     cudaError_t (*integrate_grp)(const void* gtab, int method, int lanes, const LaunchCtx&, const uint32_t*, int64_t,
                                  int, int, int, int grid, cudaStream_t);
     int (*blocks_per_sm)(int method, int dae);
@@ -191,19 +191,19 @@ struct MechOps {
     // ---- integration launchers (defined in chem_launch_impl.cuh, instantiated in launch_*.cu)
     template <bool DAE>
     static cudaError_t lock_t(const P& p, int method, const LaunchCtx& L, const uint32_t* ids, int64_t n, int kmax,
-                              int fin, int nsm, cudaStream_t s)
+                              int refill, int fin, int nsm, cudaStream_t s)
     {
-        if (method == CHEM_METHOD_RODAS3) return Launch<M, Rodas3, DAE>::lock(p, L, ids, n, kmax, fin, nsm, s);
-        if (method == CHEM_METHOD_ROS4) return Launch<M, Ros4, DAE>::lock(p, L, ids, n, kmax, fin, nsm, s);
-        return Launch<M, Rodas4, DAE>::lock(p, L, ids, n, kmax, fin, nsm, s);
+        if (method == CHEM_METHOD_RODAS3) return Launch<M, Rodas3, DAE>::lock(p, L, ids, n, kmax, refill, fin, nsm, s);
+        if (method == CHEM_METHOD_ROS4) return Launch<M, Ros4, DAE>::lock(p, L, ids, n, kmax, refill, fin, nsm, s);
+        return Launch<M, Rodas4, DAE>::lock(p, L, ids, n, kmax, refill, fin, nsm, s);
     }
-    // lockstep bulk launch (chem_opts.lockstep); Rosenbrock methods only
+    // lockstep launch (chem_opts.lockstep / lockstep_sparse); Rosenbrock methods only
     static cudaError_t integrate_lock(const void* pp, int method, int dae, const LaunchCtx& L, const uint32_t* ids,
-                                      int64_t n, int kmax, int fin, int nsm, cudaStream_t s)
+                                      int64_t n, int kmax, int refill, int fin, int nsm, cudaStream_t s)
     {
         const P& p = *static_cast<const P*>(pp);
-        return dae ? lock_t<true>(p, method, L, ids, n, kmax, fin, nsm, s)
-                   : lock_t<false>(p, method, L, ids, n, kmax, fin, nsm, s);
+        return dae ? lock_t<true>(p, method, L, ids, n, kmax, refill, fin, nsm, s)
+                   : lock_t<false>(p, method, L, ids, n, kmax, refill, fin, nsm, s);
     }
     template <bool DAE>
     static cudaError_t integrate_t(const P& p, int method, const LaunchCtx& L, const uint32_t* ids, int64_t n,
@@ -432,6 +432,7 @@ void chem_default_opts(chem_opts* o)
     o->h0_factor = 0.01;
     o->lockstep = 2;
     o->kmax_first = 1;
+    o->lockstep_sparse = 0;
 }
 
 const char* chem_strerror(int code)
@@ -453,7 +454,7 @@ static int check_opts(const chem_opts* o)
         (o->method < CHEM_METHOD_RODAS4 || o->method > CHEM_METHOD_ROS4) ||
         !std::isfinite(o->T_min) || !(o->eps_change > 0.0 && o->eps_change <= 1.0) ||
         (o->temperature_mode != 0 && o->temperature_mode != 1) || (o->refill_bulk != 0 && o->refill_bulk != 1) ||
-        o->lockstep < 0 || o->lockstep > 2 || o->kmax_first < 0 ||
+        o->lockstep < 0 || o->lockstep > 2 || o->kmax_first < 0 || o->lockstep_sparse < 0 || o->lockstep_sparse > 1 ||
         !(o->h0_factor > 0.0 && o->h0_factor <= 1.0) ||
         (o->lanes_per_cell != 1 && o->lanes_per_cell != 4 && o->lanes_per_cell != 8))
         return CHEM_EINVAL;
@@ -737,7 +738,7 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
             CK(ops.integrate_grp(c->d_gtab, o.method, o.lanes_per_cell, L, lst, nl, kmax_b, 0, 0,
                                  (int)((nl * o.lanes_per_cell + kGrpBS - 1) / kGrpBS), s));
         else if (lock)
-            CK(ops.integrate_lock(c->params.data(), o.method, o.temperature_mode, L, lst, nl, kmax_b, 0, c->num_sms,
+            CK(ops.integrate_lock(c->params.data(), o.method, o.temperature_mode, L, lst, nl, kmax_b, 0, 0, c->num_sms,
                                   s));
         else if (o.refill_bulk) {
             // persistent grid; a lane whose cell finishes its burst early takes the next id
@@ -790,6 +791,10 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
             const int grid = std::max(1, std::min<int>(c->num_sms * ops.grp_blocks_per_sm(o.method, o.lanes_per_cell),
                                                        (int)((n_cur + cells_per_block - 1) / cells_per_block)));
             CK(ops.integrate_grp(c->d_gtab, o.method, o.lanes_per_cell, L, cur, n_cur, o.kmax_sparse, 1, 1, grid, s));
+        } else if (o.lockstep_sparse && o.method != CHEM_METHOD_EXPLICIT) {
+            // persistent lockstep blocks (one per SM) with warp-batched refill
+            CK(ops.integrate_lock(c->params.data(), o.method, o.temperature_mode, L, cur, n_cur, o.kmax_sparse, 1, 1,
+                                  c->num_sms, s));
         } else {
             const int grid = std::max(1, std::min<int>(c->num_sms * ops.blocks_per_sm(o.method, o.temperature_mode),
                                                        (int)((n_cur + kIntegrateBS - 1) / kIntegrateBS)));

@@ -664,12 +664,12 @@ __global__ void __launch_bounds__(BS) k_integrate(const __grid_constant__ Params
     constexpr unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     for (;;) {
-        if (!LOCK && refill) {
+        if (refill) {
             // Persistent lane refill, batched per warp: idle lanes wait until a quarter of the warp
             // is idle (or nothing runs), then take consecutive list entries with one warp-aggregated
             // atomic and load them together, so the dependent-load latency of a cell load is paid
             // once per batch instead of once per finished lane.  All 32 lanes stay in the loop until
-            // the warp's work is exhausted (the ballots name the full warp).
+            // the warp's (LOCK: the block's) work is exhausted (the ballots name the full warp).
             for (;;) {
                 const unsigned need = __ballot_sync(FULL, !have && live);
                 if (need == 0) break;
@@ -685,7 +685,14 @@ __global__ void __launch_bounds__(BS) k_integrate(const __grid_constant__ Params
                     else take(idx);
                 }
             }
-            if (!__any_sync(FULL, have)) break;
+            if constexpr (LOCK) {
+                // lockstep refill (chem_opts.lockstep_sparse): the block's warps take each substep
+                // together; the block leaves when none of its threads holds a cell (the cursor is
+                // exhausted for every idle lane, or it would have fetched one above)
+                if (!__syncthreads_or(have)) break;
+            } else {
+                if (!__any_sync(FULL, have)) break;
+            }
             if (!have) continue;
         } else {
             while (!have && live) {

@@ -19,7 +19,7 @@ struct Launch {
                            int refill, int fin, int grid, cudaStream_t s);
     // lockstep bulk launch: persistent blocks, one per SM (chem_opts.lockstep)
     static cudaError_t lock(const Params<M>& p, const LaunchCtx& L, const uint32_t* ids, int64_t n, int kmax,
-                            int fin, int nsm, cudaStream_t s);
+                            int refill, int fin, int nsm, cudaStream_t s);
     static int blocks_per_sm();
     static constexpr size_t smem() { return (size_t)SmemLayout<M, Meth, DAE>::bytes_per_thread * kIntegrateBS; }
 };

@@ -38,7 +38,7 @@ cudaError_t Launch<M, Meth, DAE>::run(const Params<M>& p, const LaunchCtx& L, co
 
 template <class M, class Meth, bool DAE>
 cudaError_t Launch<M, Meth, DAE>::lock(const Params<M>& p, const LaunchCtx& L, const uint32_t* ids, int64_t n,
-                                       int kmax, int fin, int nsm, cudaStream_t s)
+                                       int kmax, int refill, int fin, int nsm, cudaStream_t s)
 {
     // persistent: one block per SM walks tiles blockIdx.x, blockIdx.x + gridDim.x, ...
     constexpr size_t b = SmemLayout<M, Meth, DAE>::bytes_per_thread;
@@ -49,7 +49,7 @@ cudaError_t Launch<M, Meth, DAE>::lock(const Params<M>& p, const LaunchCtx& L, c
     cudaError_t e = set_smem_once(done_dev, kern, sm);
     if (e != cudaSuccess) return e;
     const int grid = (int)std::min<int64_t>((n + BS - 1) / BS, nsm);
-    kern<<<grid, BS, sm, s>>>(p, L, ids, n, kmax, 0, fin);
+    kern<<<grid, BS, sm, s>>>(p, L, ids, n, kmax, refill, fin);
     return cudaGetLastError();
 }
 
