@@ -469,7 +469,7 @@ def ours(args):
                        "active0": s0["active0"], "t_gate_ms": s0["t_gate_ms"], "t_compact_ms": s0["t_compact_ms"],
                        "t_sparse_ms": s0["t_sparse_ms"], "n_unfinished": s0["n_unfinished"],
                        "n_nonfinite": s0["n_nonfinite"], "max_energy_drift": s0["max_energy_drift"],
-                       "lockstep": s0["lockstep"],
+                       "lockstep": s0["lockstep"], "lpt": s0.get("lpt", 0),
                        "bulk_simt_eff": s0["bulk_substeps"] / max(32 * s0["warp_substeps"], 1)},
         }
         print(json.dumps(line))

@@ -112,11 +112,18 @@ typedef struct {
     int32_t lockstep_sparse; /* the sparse launch as persistent 256-thread blocks with one barrier per
                                substep and warp-batched lane refill (the lockstep of the bulk bursts
                                applied to the tail): 0 off, 1 on.  Bitwise-neutral.               */
+    int32_t schedule_lpt;   /* heavy-first schedule: the active list sorted by the previous call's
+                               per-cell substeps (kept in the workspace; used only when this call
+                               integrates the same cell layout) and run as one persistent lockstep
+                               launch, longest cells first: 0 off, 1 on, 2 auto (on when cells above
+                               64 substeps carried at least half of the previous call's work).
+                               Bitwise-neutral.                                                    */
 } chem_opts;
 
 /* fills the paper's defaults: 500 K, 5, 1e4, 1e5, 1e-6 K, RODAS4, compact_bulk = 1, lanes_per_cell = 1,
    eps_change = 0.01, temperature_mode = 0,
-   refill_bulk = 0, h0_factor = 0.01, lockstep = 2 (auto), kmax_first = 1, lockstep_sparse = 0 */
+   refill_bulk = 0, h0_factor = 0.01, lockstep = 2 (auto), kmax_first = 1, lockstep_sparse = 0,
+   schedule_lpt = 2 (auto) */
 void chem_default_opts(chem_opts* o);
 
 /* ---- one AMR box / grid (FAB analogue) for the fused multi-box call ----------------- */
@@ -151,6 +158,7 @@ typedef struct {
                                    bulk lane substeps / (32 x warp_substeps))                   */
     int64_t bulk_substeps;      /* lane substeps attempted in bulk launches                     */
     int64_t lockstep;           /* 1: this call's bulk bursts ran in lockstep                   */
+    int64_t lpt;                /* 1: this call ran the heavy-first schedule (schedule_lpt)      */
 } chem_stats;
 
 typedef struct chem_ctx chem_ctx;   /* opaque, library-owned */

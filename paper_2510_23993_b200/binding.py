@@ -46,7 +46,7 @@ class ChemOpts(ctypes.Structure):
                 ("compact_bulk", ctypes.c_int32), ("lanes_per_cell", ctypes.c_int32),
                 ("eps_change", ctypes.c_double), ("temperature_mode", ctypes.c_int32),
                 ("refill_bulk", ctypes.c_int32), ("h0_factor", ctypes.c_double), ("lockstep", ctypes.c_int32),
-                ("kmax_first", ctypes.c_int32), ("lockstep_sparse", ctypes.c_int32)]
+                ("kmax_first", ctypes.c_int32), ("lockstep_sparse", ctypes.c_int32), ("schedule_lpt", ctypes.c_int32)]
 
 
 class ChemBox(ctypes.Structure):
@@ -61,7 +61,7 @@ class ChemStats(ctypes.Structure):
         "jac_evals", "lu_count", "n_unfinished", "n_newton_fail", "n_nonfinite", "n_T_range")] + [
         (n, ctypes.c_double) for n in ("t_gate_ms", "t_bulk_ms", "t_compact_ms", "t_sparse_ms",
                                        "max_energy_drift")] + [("active_per_iter", ctypes.c_int64 * 16)] + [
-        (n, ctypes.c_int64) for n in ("warp_substeps", "bulk_substeps", "lockstep")]
+        (n, ctypes.c_int64) for n in ("warp_substeps", "bulk_substeps", "lockstep", "lpt")]
 
     def to_dict(self):
         d = {n: getattr(self, n) for n, _ in self._fields_ if n != "active_per_iter"}

@@ -14,6 +14,8 @@
 #include "chem_group.cuh"
 #include "chem_launch.cuh"
 
+#include <cub/device/device_radix_sort.cuh>
+
 using namespace chem;
 
 namespace {
@@ -334,7 +336,7 @@ int validate(const chem_mech_desc* d)
 
 // ------------------------------------------------------------------ workspace layout
 struct WsLayout {
-    size_t stats, boxes, start, cell_t, cell_h, steps, box, state, ids0, idsA, idsB, total;
+    size_t stats, boxes, start, cell_t, cell_h, steps, box, state, ids0, idsA, idsB, key0, key1, total;
 };
 
 inline size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -354,6 +356,8 @@ WsLayout ws_layout(int64_t N, int32_t B)
     w.ids0 = o; o = al256(o + (size_t)N * 4);
     w.idsA = o; o = al256(o + (size_t)N * 4);
     w.idsB = o; o = al256(o + (size_t)N * 4);
+    w.key0 = o; o = al256(o + (size_t)N * 4);     // heavy-first schedule: cost hints and their sort buffer
+    w.key1 = o; o = al256(o + (size_t)N * 4);
     w.total = o;
     return w;
 }
@@ -378,6 +382,11 @@ struct chem_ctx {
     int32_t* trace = nullptr;        // device [trace_rows][nboxes] activity trace (App. B), or null
     int32_t trace_rows = 0;
     double simt_eff = 1.0;           // bulk SIMT efficiency of the last call (lockstep = 2 input)
+    void* sort_tmp = nullptr;        // cub radix-sort scratch of the heavy-first schedule (library-owned)
+    size_t sort_tmp_bytes = 0;
+    int64_t last_total = -1;         // layout of the previous call: the workspace's per-cell substep
+    int32_t last_nboxes = -1;        //   counts are a cost hint for this call only if it matches
+    const void* last_rho0 = nullptr;
 };
 
 namespace {
@@ -433,6 +442,7 @@ void chem_default_opts(chem_opts* o)
     o->lockstep = 2;
     o->kmax_first = 1;
     o->lockstep_sparse = 0;
+    o->schedule_lpt = 2;
 }
 
 const char* chem_strerror(int code)
@@ -454,7 +464,7 @@ static int check_opts(const chem_opts* o)
         (o->method < CHEM_METHOD_RODAS4 || o->method > CHEM_METHOD_ROS4) ||
         !std::isfinite(o->T_min) || !(o->eps_change > 0.0 && o->eps_change <= 1.0) ||
         (o->temperature_mode != 0 && o->temperature_mode != 1) || (o->refill_bulk != 0 && o->refill_bulk != 1) ||
-        o->lockstep < 0 || o->lockstep > 2 || o->kmax_first < 0 || o->lockstep_sparse < 0 || o->lockstep_sparse > 1 ||
+        o->lockstep < 0 || o->lockstep > 2 || o->kmax_first < 0 || o->lockstep_sparse < 0 || o->lockstep_sparse > 1 || o->schedule_lpt < 0 || o->schedule_lpt > 2 ||
         !(o->h0_factor > 0.0 && o->h0_factor <= 1.0) ||
         (o->lanes_per_cell != 1 && o->lanes_per_cell != 4 && o->lanes_per_cell != 8))
         return CHEM_EINVAL;
@@ -515,6 +525,7 @@ void chem_finalize(chem_ctx* c)
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
     if (c->d_gtab) cudaFree(c->d_gtab);
+    if (c->sort_tmp) cudaFree(c->sort_tmp);
     delete c;
 }
 
@@ -694,7 +705,15 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
 
     // ---- Alg. 3 §1: gate + count + index map
     CK(cudaEventRecord(c->ev[0], s));
-    k_gate<kStreamBS><<<grid_for(total, kStreamBS), kStreamBS, 0, s>>>(L, ids0);
+    uint32_t* key0 = reinterpret_cast<uint32_t*>(base + W.key0);
+    uint32_t* key1 = reinterpret_cast<uint32_t*>(base + W.key1);
+    // the previous call's per-cell substep counts are this call's cost hints only if it integrated
+    // the same cell layout (same total, box count and first box)
+    const bool history = total == c->last_total && nboxes == c->last_nboxes && boxes[0].rho == c->last_rho0;
+    c->last_total = total;
+    c->last_nboxes = nboxes;
+    c->last_rho0 = boxes[0].rho;
+    k_gate<kStreamBS><<<grid_for(total, kStreamBS), kStreamBS, 0, s>>>(L, ids0, key0);
     CK(cudaGetLastError());
     CK(cudaEventRecord(c->ev[1], s));
     int64_t n_active = 0;
@@ -710,10 +729,38 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
         }
     }
 
-    // ---- Alg. 3 §2: bulk bursts while N_active > N*
+    // ---- Heavy-first schedule (chem_opts.schedule_lpt).  When the cost hints say
+    // most of the work sits in heavy cells (> kHeavySteps substeps last call), the round-robin bulk
+    // bursts would start those cells' long chains late and leave them as the tail.  Instead the
+    // index map is sorted by hint, heaviest first (stable LSD radix sort: ties keep gate order), and
+    // the whole list runs as one persistent lockstep launch with warp-batched refill: the longest
+    // chains start at once and light cells fill the slots that free up (longest-processing-time
+    // first).  Per-cell arithmetic is unchanged, so results are bitwise those of the default.
+    const uint64_t pred_total = c->h_stats[S_PRED_TOTAL], pred_heavy = c->h_stats[S_PRED_HEAVY];
+    const bool lpt = n_active > 0 && !use_grp && o.method != CHEM_METHOD_EXPLICIT &&
+                     (o.schedule_lpt == 1 ||
+                      (o.schedule_lpt == 2 && history && pred_total > 0 && 2 * pred_heavy >= pred_total));
+    st.lpt = lpt;
     const uint32_t* cur = ids0;
     int64_t n_cur = n_active;
     uint32_t* nxt = idsA;
+    if (lpt) {
+        cub::DoubleBuffer<uint32_t> dk(key0, key1), dv(ids0, idsA);
+        size_t need = 0;
+        CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, need, dk, dv, (int)n_active, 0, 32, s));
+        if (need > c->sort_tmp_bytes) {
+            if (c->sort_tmp) CK(cudaFree(c->sort_tmp));
+            c->sort_tmp = nullptr;
+            c->sort_tmp_bytes = 0;
+            CK(cudaMalloc(&c->sort_tmp, need));
+            c->sort_tmp_bytes = need;
+        }
+        CK(cub::DeviceRadixSort::SortPairsDescending(c->sort_tmp, need, dk, dv, (int)n_active, 0, 32, s));
+        cur = dv.Current();
+        nxt = (cur == idsA) ? idsB : idsA;
+    }
+
+    // ---- Alg. 3 §2: bulk bursts while N_active > N*
     // lockstep bursts (chem_opts.lockstep; auto: the previous call's bulk SIMT efficiency was low)
     const bool lock = !use_grp && !o.refill_bulk && o.method != CHEM_METHOD_EXPLICIT &&
                       (o.lockstep == 1 || (o.lockstep == 2 && c->simt_eff < kLockEff));
@@ -727,7 +774,7 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
                                           (kGrpBS / o.lanes_per_cell)
                                     : (int64_t)c->num_sms * ops.blocks_per_sm(o.method, o.temperature_mode) *
                                           kIntegrateBS;
-    while (n_cur > nstar && n_cur > 0) {
+    while (!lpt && n_cur > nstar && n_cur > 0) {
         const bool first_burst = lock && st.bulk_iters == 0 && o.kmax_first > 0;
         const int kmax_b = first_burst ? o.kmax_first : o.kmax_bulk;
         const bool all_cells = !o.compact_bulk;
@@ -791,7 +838,7 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
             const int grid = std::max(1, std::min<int>(c->num_sms * ops.grp_blocks_per_sm(o.method, o.lanes_per_cell),
                                                        (int)((n_cur + cells_per_block - 1) / cells_per_block)));
             CK(ops.integrate_grp(c->d_gtab, o.method, o.lanes_per_cell, L, cur, n_cur, o.kmax_sparse, 1, 1, grid, s));
-        } else if (o.lockstep_sparse && o.method != CHEM_METHOD_EXPLICIT) {
+        } else if ((o.lockstep_sparse || lpt) && o.method != CHEM_METHOD_EXPLICIT) {
             // persistent lockstep blocks (one per SM) with warp-batched refill
             CK(ops.integrate_lock(c->params.data(), o.method, o.temperature_mode, L, cur, n_cur, o.kmax_sparse, 1, 1,
                                   c->num_sms, s));

@@ -27,7 +27,8 @@ enum CellState : uint8_t {
 
 enum StatIdx {
     S_ATTEMPTED = 0, S_ACCEPTED, S_RHS, S_JAC, S_LU, S_NEWTON_FAIL, S_NONFINITE, S_TRANGE, S_UNFINISHED,
-    S_DONE, S_DRIFT_BITS, S_COUNT_ACTIVE, S_CURSOR, S_FROZEN, S_WARP_SUBSTEPS, S_NSTATS
+    S_DONE, S_DRIFT_BITS, S_COUNT_ACTIVE, S_CURSOR, S_FROZEN, S_WARP_SUBSTEPS, S_PRED_TOTAL, S_PRED_HEAVY,
+    S_NSTATS
 };
 
 struct DevBox {
@@ -80,7 +81,8 @@ __device__ __forceinline__ void warp_add(unsigned long long* p, unsigned long lo
 // written to out[] at positions reserved with one atomicAdd per block.  Order within a block
 // follows thread order.  Requires all threads of the block to call it.
 template <int BS>
-__device__ __forceinline__ void block_compact(bool keep, uint32_t g, uint32_t* out, unsigned long long* counter)
+__device__ __forceinline__ void block_compact(bool keep, uint32_t g, uint32_t* out, unsigned long long* counter,
+                                              uint32_t key = 0, uint32_t* key_out = nullptr)
 {
     __shared__ int warp_cnt[BS / 32];
     __shared__ unsigned long long base;
@@ -95,17 +97,27 @@ __device__ __forceinline__ void block_compact(bool keep, uint32_t g, uint32_t* o
         base = s ? atomicAdd(counter, (unsigned long long)s) : 0ull;
     }
     __syncthreads();
-    if (keep) out[base + warp_cnt[wid] + __popc(bal & ((1u << lane) - 1u))] = g;
+    if (keep) {
+        const unsigned long long at = base + warp_cnt[wid] + __popc(bal & ((1u << lane) - 1u));
+        out[at] = g;
+        if (key_out) key_out[at] = key;
+    }
     __syncthreads();
 }
 
 // ----------------------------------------------------------------------------- A2 gate + count
+// keys_out (nullable): each listed cell's attempted substeps in the previous call at the same index
+// (the cost hint of the heavy-first schedule); S_PRED_TOTAL / S_PRED_HEAVY sum that hint over the
+// active cells and over those above kHeavySteps.
+constexpr uint32_t kHeavySteps = 64;
+
 template <int BS>
-__global__ void __launch_bounds__(BS) k_gate(LaunchCtx L, uint32_t* ids_out)
+__global__ void __launch_bounds__(BS) k_gate(LaunchCtx L, uint32_t* ids_out, uint32_t* keys_out)
 {
     for (int64_t base = (int64_t)blockIdx.x * BS; base < L.total; base += (int64_t)gridDim.x * BS) {
         const int64_t g = base + threadIdx.x;
         bool act = false;
+        uint32_t prev = 0;
         if (g < L.total) {
             const int b = find_box(L, g);
             const DevBox bx = L.boxes[b];
@@ -113,9 +125,15 @@ __global__ void __launch_bounds__(BS) k_gate(LaunchCtx L, uint32_t* ids_out)
             const double T = bx.T[off];
             act = (T >= L.T_min) && !(bx.solid && bx.solid[off]);   // Alg. 3 §1
             L.state[g] = act ? ST_FRESH : ST_INACTIVE;
-            if (act) { L.cell_steps[g] = 0; L.cell_box[g] = b; }
+            if (keys_out) prev = act ? (uint32_t)max(L.cell_steps[g], 0) : 0u;
+            L.cell_steps[g] = 0;
+            if (act) L.cell_box[g] = b;
         }
-        block_compact<BS>(act, (uint32_t)g, ids_out, &L.stats[S_COUNT_ACTIVE]);
+        if (keys_out) {
+            warp_add(&L.stats[S_PRED_TOTAL], prev);
+            warp_add(&L.stats[S_PRED_HEAVY], prev > kHeavySteps ? prev : 0u);
+        }
+        block_compact<BS>(act, (uint32_t)g, ids_out, &L.stats[S_COUNT_ACTIVE], prev, keys_out);
     }
 }
 

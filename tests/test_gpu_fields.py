@@ -189,14 +189,15 @@ def test_virtual_ranks_bitwise(chem, ora, doc):
 
 @pytest.mark.parametrize("opts", [dict(refill_bulk=1), dict(kmax_bulk=20, n_active_star=3000),
                                   dict(compact_bulk=0, kmax_bulk=3), dict(lockstep=1),
-                                  dict(lockstep=1, kmax_first=0, kmax_bulk=3), dict(lockstep=1, compact_bulk=0)])
+                                  dict(lockstep=1, kmax_first=0, kmax_bulk=3), dict(lockstep=1, compact_bulk=0),
+                                  dict(lockstep_sparse=1), dict(schedule_lpt=1)])
 def test_cfg3_schedule_variants_bitwise(ora, doc, opts):
     """Bulk-sparse variants (lane-refill bursts, longer bursts, the paper's all-cells bursts) give
     bitwise the same field as the default schedule (P:177 / S:191), at full cfg3 size."""
     m = ora.m
     ids = [0, 16, 32, 48]                    # the four boxes along y at x = 0 (band + spots)
     raw, _ = synth.field_cfg3(doc, m.W, m.species, device=DEV, box_ids=ids)
-    ref, st0, _ = _run(Chem("h2air_li2004", device=0, atol_T=1e-6, lockstep=0), raw)
+    ref, st0, _ = _run(Chem("h2air_li2004", device=0, atol_T=1e-6, lockstep=0, schedule_lpt=0), raw)
     alt, st1, _ = _run(Chem("h2air_li2004", device=0, atol_T=1e-6, **opts), raw)
     assert st1["lockstep"] == opts.get("lockstep", 0)
     for a, b in zip(ref, alt):
@@ -251,3 +252,28 @@ def test_host_runner_matches_device_path(chem, doc, chunks):
     assert hr.h2d_bytes == 6 * 512 * (3 + len(doc["species"])) * 8
     assert hr.d2h_bytes == 6 * 512 * (1 + len(doc["species"])) * 8
     del rng
+
+
+def test_cfg3_heavy_first_second_call_bitwise(ora, doc):
+    """Heavy-first schedule (schedule_lpt = 2): the first call has no cost hints and runs the default
+    schedule; the second call on the same layout sorts the active list by the first call's per-cell
+    substeps and runs it as one persistent lockstep launch.  Both give bitwise the default's field."""
+    m = ora.m
+    ids = [0, 16, 32, 48]
+    raw, _ = synth.field_cfg3(doc, m.W, m.species, device=DEV, box_ids=ids)
+    ref, st0, _ = _run(Chem("h2air_li2004", device=0, atol_T=1e-6, schedule_lpt=0), raw)
+    chem = Chem("h2air_li2004", device=0, atol_T=1e-6, schedule_lpt=2)
+    boxes = []
+    for b in raw:
+        e = chem.energy(b["T"], b["Y"])
+        boxes.append(Box(b["rho"], e, b["T"].clone(), b["Y"].clone(), b["dt"], b.get("solid")))
+    for call in range(2):
+        for bx, b in zip(boxes, raw):
+            bx.T.copy_(b["T"])
+            bx.Y.copy_(b["Y"])
+        st = chem.integrate_boxes(boxes, **GPU_TOL)
+        torch.cuda.synchronize()
+        assert st["lpt"] == call                       # hints exist only on the second call
+        assert st["steps_attempted"] == st0["steps_attempted"]
+        for a, b in zip(ref, boxes):
+            assert torch.equal(a.T, b.T) and torch.equal(a.Y, b.Y)
