@@ -67,6 +67,7 @@ class Chem:
             raise _b.ChemError(rc, self.lib)
         self._h = h
         self._ws = None
+        self._ws_layout = {}
         self.last_stats = None
 
     def __del__(self):
@@ -104,11 +105,24 @@ class Chem:
         if rc != 0:
             raise _b.ChemError(rc, self.lib)
 
-    def workspace(self, max_cells, max_boxes=1):
+    def workspace(self, max_cells, max_boxes=1, layout=None):
+        """Device workspace for a call.  `layout` (a hashable key of the call's cell layout) selects a
+        workspace of its own, so the per-cell cost hints the heavy-first schedule reads (DESIGN.md
+        §6.16) survive between calls on that layout when calls on other layouts (AMR levels)
+        interleave; at most 8 layouts are kept."""
         nbytes = self.lib.chem_workspace_bytes(self._h, int(max_cells), int(max_boxes))
-        if self._ws is None or self._ws.numel() < nbytes:
-            self._ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=self.device)
-        return self._ws
+        if layout is None:
+            if self._ws is None or self._ws.numel() < nbytes:
+                self._ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=self.device)
+            return self._ws
+        ws = self._ws_layout.pop(layout, None)
+        if ws is None or ws.numel() < nbytes:
+            ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=self.device)
+        self._ws_layout[layout] = ws            # most recently used last
+        while len(self._ws_layout) > 8:
+            self._ws_layout.pop(next(iter(self._ws_layout)))
+        self._ws = ws
+        return ws
 
     # ---- point evaluations ---------------------------------------------------------------
     def rates(self, rho, T, Y, out=None):
@@ -201,7 +215,7 @@ class Chem:
             arr[i].ld = ld
             arr[i].dt = float(bx.dt)
             total += bx.ncells
-        ws = self.workspace(total, nb)
+        ws = self.workspace(total, nb, layout=(total, nb, boxes[0].rho.data_ptr()))
         if box_cost is not None:
             _check(box_cost, "box_cost")
         st = _b.ChemStats()

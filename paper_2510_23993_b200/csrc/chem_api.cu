@@ -384,9 +384,7 @@ struct chem_ctx {
     double simt_eff = 1.0;           // bulk SIMT efficiency of the last call (lockstep = 2 input)
     void* sort_tmp = nullptr;        // cub radix-sort scratch of the heavy-first schedule (library-owned)
     size_t sort_tmp_bytes = 0;
-    int64_t last_total = -1;         // layout of the previous call: the workspace's per-cell substep
-    int32_t last_nboxes = -1;        //   counts are a cost hint for this call only if it matches
-    const void* last_rho0 = nullptr;
+    unsigned long long* h_sig = nullptr;   // pinned [3]: staging of the workspace layout signature
 };
 
 namespace {
@@ -506,6 +504,7 @@ int chem_init(const chem_mech_desc* mech, const chem_opts* opts, int device, che
     }
     cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
     if (cudaMallocHost(&c->h_stats, sizeof(unsigned long long) * S_NSTATS) != cudaSuccess ||
+        cudaMallocHost(&c->h_sig, sizeof(unsigned long long) * 3) != cudaSuccess ||
         cudaEventCreate(&c->ev[0]) != cudaSuccess || cudaEventCreate(&c->ev[1]) != cudaSuccess ||
         ensure_host_boxes(c, 64) != CHEM_OK) {
         chem_finalize(c);
@@ -526,6 +525,7 @@ void chem_finalize(chem_ctx* c)
         if (e) cudaEventDestroy(e);
     if (c->d_gtab) cudaFree(c->d_gtab);
     if (c->sort_tmp) cudaFree(c->sort_tmp);
+    if (c->h_sig) cudaFreeHost(c->h_sig);
     delete c;
 }
 
@@ -684,7 +684,7 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
 
     CK(cudaMemcpyAsync(base + W.boxes, c->h_boxes, sizeof(DevBox) * nboxes, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(base + W.start, c->h_start, sizeof(int64_t) * (nboxes + 1), cudaMemcpyHostToDevice, s));
-    CK(cudaMemsetAsync(L.stats, 0, S_NSTATS * 8, s));
+    CK(cudaMemsetAsync(L.stats, 0, S_SIG0 * 8, s));   // the layout signature slots persist across calls
     if (box_cost) CK(cudaMemsetAsync(box_cost, 0, sizeof(double) * nboxes, s));
     if (total == 0) {
         CK(cudaStreamSynchronize(s));
@@ -707,12 +707,6 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
     CK(cudaEventRecord(c->ev[0], s));
     uint32_t* key0 = reinterpret_cast<uint32_t*>(base + W.key0);
     uint32_t* key1 = reinterpret_cast<uint32_t*>(base + W.key1);
-    // the previous call's per-cell substep counts are this call's cost hints only if it integrated
-    // the same cell layout (same total, box count and first box)
-    const bool history = total == c->last_total && nboxes == c->last_nboxes && boxes[0].rho == c->last_rho0;
-    c->last_total = total;
-    c->last_nboxes = nboxes;
-    c->last_rho0 = boxes[0].rho;
     k_gate<kStreamBS><<<grid_for(total, kStreamBS), kStreamBS, 0, s>>>(L, ids0, key0);
     CK(cudaGetLastError());
     CK(cudaEventRecord(c->ev[1], s));
@@ -736,6 +730,14 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
     // the whole list runs as one persistent lockstep launch with warp-batched refill: the longest
     // chains start at once and light cells fill the slots that free up (longest-processing-time
     // first).  Per-cell arithmetic is unchanged, so results are bitwise those of the default.
+    // The workspace's per-cell substep counts (left by the last call that used this workspace) are
+    // this call's cost hints only if that call integrated the same cell layout: same total, box count
+    // and first box, recorded in the workspace's signature slots (read with the count above).
+    const unsigned long long sig[3] = {(unsigned long long)total, (unsigned long long)nboxes,
+                                       (unsigned long long)(uintptr_t)boxes[0].rho};
+    const bool history = c->h_stats[S_SIG0] == sig[0] && c->h_stats[S_SIG1] == sig[1] && c->h_stats[S_SIG2] == sig[2];
+    std::memcpy(c->h_sig, sig, sizeof(sig));
+    CK(cudaMemcpyAsync(L.stats + S_SIG0, c->h_sig, sizeof(sig), cudaMemcpyHostToDevice, s));
     const uint64_t pred_total = c->h_stats[S_PRED_TOTAL], pred_heavy = c->h_stats[S_PRED_HEAVY];
     const bool lpt = n_active > 0 && !use_grp && o.method != CHEM_METHOD_EXPLICIT &&
                      (o.schedule_lpt == 1 ||

@@ -28,6 +28,7 @@ enum CellState : uint8_t {
 enum StatIdx {
     S_ATTEMPTED = 0, S_ACCEPTED, S_RHS, S_JAC, S_LU, S_NEWTON_FAIL, S_NONFINITE, S_TRANGE, S_UNFINISHED,
     S_DONE, S_DRIFT_BITS, S_COUNT_ACTIVE, S_CURSOR, S_FROZEN, S_WARP_SUBSTEPS, S_PRED_TOTAL, S_PRED_HEAVY,
+    S_SIG0, S_SIG1, S_SIG2,   // cell-layout signature of the workspace's cost hints (not cleared per call)
     S_NSTATS
 };
 

@@ -255,9 +255,10 @@ def test_host_runner_matches_device_path(chem, doc, chunks):
 
 
 def test_cfg3_heavy_first_second_call_bitwise(ora, doc):
-    """Heavy-first schedule (schedule_lpt = 2): the first call has no cost hints and runs the default
-    schedule; the second call on the same layout sorts the active list by the first call's per-cell
-    substeps and runs it as one persistent lockstep launch.  Both give bitwise the default's field."""
+    """Heavy-first schedule (schedule_lpt = 2): the second call on the same layout sorts the active list
+    by the first call's per-cell substeps and runs it as one persistent lockstep launch (the first
+    call may or may not find hints: a recycled workspace block can carry a signature of the same
+    layout).  Every call gives bitwise the default schedule's field."""
     m = ora.m
     ids = [0, 16, 32, 48]
     raw, _ = synth.field_cfg3(doc, m.W, m.species, device=DEV, box_ids=ids)
@@ -273,7 +274,8 @@ def test_cfg3_heavy_first_second_call_bitwise(ora, doc):
             bx.Y.copy_(b["Y"])
         st = chem.integrate_boxes(boxes, **GPU_TOL)
         torch.cuda.synchronize()
-        assert st["lpt"] == call                       # hints exist only on the second call
+        if call == 1:
+            assert st["lpt"] == 1                      # the first call left hints for this layout
         assert st["steps_attempted"] == st0["steps_attempted"]
         for a, b in zip(ref, boxes):
             assert torch.equal(a.T, b.T) and torch.equal(a.Y, b.Y)
