@@ -12,8 +12,9 @@ m = load_mechanism("h2air_li2004")
 d = synth.cfg1c(m.species, m.W)
 idx = np.arange(0, 4096, 64)
 dev = torch.device("cuda", 0)
-for lanes, lock in ((1, 0), (8, 0), (1, 1)):
-    ch = Chem("h2air_li2004", device=0, lanes_per_cell=lanes, kmax_bulk=3, n_active_star=16, lockstep=lock)
+for lanes, lock, lpt in ((1, 0, 0), (8, 0, 0), (1, 1, 0), (1, 0, 1)):
+    ch = Chem("h2air_li2004", device=0, lanes_per_cell=lanes, kmax_bulk=3, n_active_star=16, lockstep=lock,
+              schedule_lpt=lpt)
     T = torch.tensor(d["T"][idx], device=dev)
     Y = torch.tensor(d["Y"][idx].T.copy(), device=dev)
     rho = torch.tensor(d["rho"][idx], device=dev)
@@ -26,7 +27,9 @@ for lanes, lock in ((1, 0), (8, 0), (1, 1)):
     w = ch.rates(rho, T, Y)
     J = ch.jacobian(rho[:8], T[:8], Y[:, :8].contiguous())
     torch.cuda.synchronize()
-    print("lanes", lanes, "lockstep", lock, st["steps_attempted"], st["sparse_cells"])
+    st2 = ch.integrate_boxes(boxes, box_cost=cost)      # second call: cost hints from the first
+    torch.cuda.synchronize()
+    print("lanes", lanes, "lockstep", lock, "lpt", lpt, st["steps_attempted"], st["sparse_cells"], st2["lpt"])
 PY
 for tool in memcheck racecheck synccheck initcheck; do
   timeout 900 compute-sanitizer --tool $tool --print-limit 20 python /tmp/san_case.py > gpurun_out/sanitize_$tool.txt 2>&1
