@@ -453,7 +453,10 @@ def ours(args):
                        "lanes_per_cell": args.lanes, "temperature_mode": args.tmode, "h0_factor": args.h0,
                        **({"opts": args.opt} if args.opt else {}),
                        "l2": "inputs >= 369 MB/GPU > 126 MB L2 (no flush needed)",
-                       "parallelism": f"boxes over {world} rank(s)", **wl.extra},
+                       "parallelism": f"boxes over {world} rank(s)",
+                       "schedule": ("heavy-first (cost hints: the previous step's per-cell substeps; the "
+                                    "warm-up steps seed them)" if s0.get("lpt") else "bulk-sparse (Alg. 3)"),
+                       **wl.extra},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": traffic, "traffic_unit": "bytes per launch (ncu)",
                          "ncu_fp64_pipe_pct": ncu_pipe,

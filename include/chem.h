@@ -174,7 +174,10 @@ const char* chem_structure_name(const chem_ctx* ctx);
 int chem_set_opts(chem_ctx* ctx, const chem_opts* opts);
 
 /* Device workspace (bytes, 256-aligned pointer) a chem_integrate* call needs for up to
- * max_cells cells in up to max_boxes boxes.  Owned by the caller (e.g. torch.empty). */
+ * max_cells cells in up to max_boxes boxes.  Owned by the caller (e.g. torch.zeros).  Zero-fill it
+ * before its first use: it carries the per-cell cost hints of the heavy-first schedule
+ * (chem_opts.schedule_lpt) from one call to the next on the same cell layout.  Results never depend
+ * on its previous contents (only the processing order does). */
 size_t chem_workspace_bytes(const chem_ctx* ctx, int64_t max_cells, int32_t max_boxes);
 
 /* Molar production rates Omega.  wdot is [ns][ld].  Never synchronises. */

@@ -113,11 +113,11 @@ class Chem:
         nbytes = self.lib.chem_workspace_bytes(self._h, int(max_cells), int(max_boxes))
         if layout is None:
             if self._ws is None or self._ws.numel() < nbytes:
-                self._ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=self.device)
+                self._ws = torch.zeros(max(nbytes, 1), dtype=torch.uint8, device=self.device)
             return self._ws
         ws = self._ws_layout.pop(layout, None)
         if ws is None or ws.numel() < nbytes:
-            ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=self.device)
+            ws = torch.zeros(max(nbytes, 1), dtype=torch.uint8, device=self.device)
         self._ws_layout[layout] = ws            # most recently used last
         while len(self._ws_layout) > 8:
             self._ws_layout.pop(next(iter(self._ws_layout)))

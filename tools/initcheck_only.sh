@@ -1,0 +1,33 @@
+#!/bin/bash
+mkdir -p gpurun_out
+cat > /tmp/san_case.py <<'PY'
+import sys, os
+sys.path.insert(0, os.getcwd())
+import numpy as np, torch, synth
+from paper_2510_23993_b200 import Chem, Box
+from paper_2510_23993_b200 import load_mechanism
+m = load_mechanism("h2air_li2004")
+d = synth.cfg1c(m.species, m.W)
+idx = np.arange(0, 4096, 64)
+dev = torch.device("cuda", 0)
+for lanes, lock, lpt in ((1, 0, 0), (8, 0, 0), (1, 1, 0), (1, 0, 1)):
+    ch = Chem("h2air_li2004", device=0, lanes_per_cell=lanes, kmax_bulk=3, n_active_star=16, lockstep=lock,
+              schedule_lpt=lpt)
+    T = torch.tensor(d["T"][idx], device=dev)
+    Y = torch.tensor(d["Y"][idx].T.copy(), device=dev)
+    rho = torch.tensor(d["rho"][idx], device=dev)
+    e = ch.energy(T, Y)
+    cost = torch.zeros(2, dtype=torch.float64, device=dev)
+    n = len(idx) // 2
+    boxes = [Box(rho[:n], e[:n], T[:n].clone(), Y[:, :n].contiguous(), 1e-6),
+             Box(rho[n:], e[n:], T[n:].clone(), Y[:, n:].contiguous(), 1e-5)]
+    st = ch.integrate_boxes(boxes, box_cost=cost)
+    w = ch.rates(rho, T, Y)
+    J = ch.jacobian(rho[:8], T[:8], Y[:, :8].contiguous())
+    torch.cuda.synchronize()
+    st2 = ch.integrate_boxes(boxes, box_cost=cost)      # second call: cost hints from the first
+    torch.cuda.synchronize()
+    print("lanes", lanes, "lockstep", lock, "lpt", lpt, st["steps_attempted"], st["sparse_cells"], st2["lpt"])
+PY
+timeout 900 compute-sanitizer --tool initcheck --print-limit 5 python /tmp/san_case.py > gpurun_out/initcheck2.txt 2>&1
+grep -E "^lanes|SUMMARY" gpurun_out/initcheck2.txt
