@@ -158,7 +158,8 @@ typedef struct {
                                    bulk lane substeps / (32 x warp_substeps))                   */
     int64_t bulk_substeps;      /* lane substeps attempted in bulk launches                     */
     int64_t lockstep;           /* 1: this call's bulk bursts ran in lockstep                   */
-    int64_t lpt;                /* 1: this call ran the heavy-first schedule (schedule_lpt)      */
+    int64_t lpt;                /* 1: this call ran the heavy-first schedule (schedule_lpt);
+                                   2: its bulk list was sorted by the cost hints (auto mode)        */
 } chem_stats;
 
 typedef struct chem_ctx chem_ctx;   /* opaque, library-owned */

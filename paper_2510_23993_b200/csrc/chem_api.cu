@@ -743,13 +743,24 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
                      (o.schedule_lpt == 1 ||
                       (o.schedule_lpt == 2 && history && pred_total > 0 && 2 * pred_heavy >= pred_total));
     st.lpt = lpt;
+    // Without the heavy-first launch, the hints still sort the bulk bursts' list (descending) when the
+    // cells' costs differ (pred max above the mean): warps then hold cells that need similar numbers
+    // of substeps (fewer idle lanes per burst) and heavy cells start first.
+    const uint64_t pred_max = c->h_stats[S_PRED_MAX];
+    const bool sort_bulk_ = !lpt && history && n_active > 0 && o.schedule_lpt == 2 && !use_grp &&
+                           o.method != CHEM_METHOD_EXPLICIT && pred_total > 0 &&
+                           (double)pred_max * (double)n_active > 1.5 * (double)pred_total;
+    const bool sort_bulk = sort_bulk_;
+    if (sort_bulk) st.lpt = 2;
     const uint32_t* cur = ids0;
     int64_t n_cur = n_active;
     uint32_t* nxt = idsA;
-    if (lpt) {
+    if (lpt || sort_bulk) {
         cub::DoubleBuffer<uint32_t> dk(key0, key1), dv(ids0, idsA);
         size_t need = 0;
-        CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, need, dk, dv, (int)n_active, 0, 32, s));
+        int bits = 1;                                    // keys <= pred_max: sort only the bits in use
+        while (bits < 32 && (1ull << bits) <= pred_max) ++bits;
+        CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, need, dk, dv, (int)n_active, 0, bits, s));
         if (need > c->sort_tmp_bytes) {
             if (c->sort_tmp) CK(cudaFree(c->sort_tmp));
             c->sort_tmp = nullptr;
@@ -757,7 +768,7 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
             CK(cudaMalloc(&c->sort_tmp, need));
             c->sort_tmp_bytes = need;
         }
-        CK(cub::DeviceRadixSort::SortPairsDescending(c->sort_tmp, need, dk, dv, (int)n_active, 0, 32, s));
+        CK(cub::DeviceRadixSort::SortPairsDescending(c->sort_tmp, need, dk, dv, (int)n_active, 0, bits, s));
         cur = dv.Current();
         nxt = (cur == idsA) ? idsB : idsA;
     }

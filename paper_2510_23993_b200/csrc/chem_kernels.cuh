@@ -28,6 +28,7 @@ enum CellState : uint8_t {
 enum StatIdx {
     S_ATTEMPTED = 0, S_ACCEPTED, S_RHS, S_JAC, S_LU, S_NEWTON_FAIL, S_NONFINITE, S_TRANGE, S_UNFINISHED,
     S_DONE, S_DRIFT_BITS, S_COUNT_ACTIVE, S_CURSOR, S_FROZEN, S_WARP_SUBSTEPS, S_PRED_TOTAL, S_PRED_HEAVY,
+    S_PRED_MAX,
     S_SIG0, S_SIG1, S_SIG2,   // cell-layout signature of the workspace's cost hints (not cleared per call)
     S_NSTATS
 };
@@ -133,6 +134,10 @@ __global__ void __launch_bounds__(BS) k_gate(LaunchCtx L, uint32_t* ids_out, uin
         if (keys_out) {
             warp_add(&L.stats[S_PRED_TOTAL], prev);
             warp_add(&L.stats[S_PRED_HEAVY], prev > kHeavySteps ? prev : 0u);
+            unsigned mx = prev;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            if ((threadIdx.x & 31) == 0 && mx) atomicMax(&L.stats[S_PRED_MAX], (unsigned long long)mx);
         }
         block_compact<BS>(act, (uint32_t)g, ids_out, &L.stats[S_COUNT_ACTIVE], prev, keys_out);
     }
