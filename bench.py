@@ -454,8 +454,10 @@ def ours(args):
                        **({"opts": args.opt} if args.opt else {}),
                        "l2": "inputs >= 369 MB/GPU > 126 MB L2 (no flush needed)",
                        "parallelism": f"boxes over {world} rank(s)",
-                       "schedule": ("heavy-first (cost hints: the previous step's per-cell substeps; the "
-                                    "warm-up steps seed them)" if s0.get("lpt") else "bulk-sparse (Alg. 3)"),
+                       "schedule": {1: "heavy-first (cost hints: the previous step's per-cell substeps; "
+                                       "the warm-up steps seed them)",
+                                    2: "bulk-sparse (Alg. 3), bulk list sorted by the previous step's "
+                                       "per-cell substeps"}.get(s0.get("lpt", 0), "bulk-sparse (Alg. 3)"),
                        **wl.extra},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": traffic, "traffic_unit": "bytes per launch (ncu)",
