@@ -739,7 +739,8 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
     std::memcpy(c->h_sig, sig, sizeof(sig));
     CK(cudaMemcpyAsync(L.stats + S_SIG0, c->h_sig, sizeof(sig), cudaMemcpyHostToDevice, s));
     const uint64_t pred_total = c->h_stats[S_PRED_TOTAL], pred_heavy = c->h_stats[S_PRED_HEAVY];
-    const bool lpt = n_active > 0 && !use_grp && o.method != CHEM_METHOD_EXPLICIT &&
+    const bool sortable = n_active > 0 && n_active <= (int64_t)0x7fffffff;   // cub's int item count
+    const bool lpt = sortable && !use_grp && o.method != CHEM_METHOD_EXPLICIT &&
                      (o.schedule_lpt == 1 ||
                       (o.schedule_lpt == 2 && history && pred_total > 0 && 2 * pred_heavy >= pred_total));
     st.lpt = lpt;
@@ -747,7 +748,7 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
     // cells' costs differ (pred max above the mean): warps then hold cells that need similar numbers
     // of substeps (fewer idle lanes per burst) and heavy cells start first.
     const uint64_t pred_max = c->h_stats[S_PRED_MAX];
-    const bool sort_bulk_ = !lpt && history && n_active > 0 && o.schedule_lpt == 2 && !use_grp &&
+    const bool sort_bulk_ = !lpt && history && sortable && o.schedule_lpt == 2 && !use_grp &&
                            o.method != CHEM_METHOD_EXPLICIT && pred_total > 0 &&
                            (double)pred_max * (double)n_active > 1.5 * (double)pred_total;
     const bool sort_bulk = sort_bulk_;
