@@ -47,6 +47,8 @@ def test_default_opts_are_the_papers():
     # P:179 K_max = 5, P:181 N* (default < 0: one resident wave of the integration kernel)
     assert (o.kmax_bulk, o.n_active_star, o.kmax_sparse, o.T_min) == (5, -1, 100000, 500.0)
     assert (o.lockstep, o.kmax_first, o.refill_bulk, o.compact_bulk) == (2, 1, 0, 1)
+    # heavy-first / sorted-bulk schedule on cost hints: auto; lockstep sparse launch: off
+    assert (o.schedule_lpt, o.lockstep_sparse) == (2, 0)
 
 
 def test_opts_struct_matches_header():
