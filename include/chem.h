@@ -115,9 +115,10 @@ typedef struct {
     int32_t schedule_lpt;   /* heavy-first schedule: the active list sorted by the previous call's
                                per-cell substeps (kept in the workspace; used only when this call
                                integrates the same cell layout) and run as one persistent lockstep
-                               launch, longest cells first: 0 off, 1 on, 2 auto (on when cells above
-                               64 substeps carried at least half of the previous call's work).
-                               Bitwise-neutral.                                                    */
+                               launch, longest cells first: 0 off, 1 on, 2 auto (on when the hints
+                               are skewed: cells above 64 substeps carried half of the previous call's
+                               work, or the largest hint exceeds 1.5x the mean), 3 keep Alg. 3's bulk
+                               bursts but over the hint-sorted list.  Bitwise-neutral.              */
 } chem_opts;
 
 /* fills the paper's defaults: 500 K, 5, 1e4, 1e5, 1e-6 K, RODAS4, compact_bulk = 1, lanes_per_cell = 1,
@@ -159,7 +160,7 @@ typedef struct {
     int64_t bulk_substeps;      /* lane substeps attempted in bulk launches                     */
     int64_t lockstep;           /* 1: this call's bulk bursts ran in lockstep                   */
     int64_t lpt;                /* 1: this call ran the heavy-first schedule (schedule_lpt);
-                                   2: its bulk list was sorted by the cost hints (auto mode)        */
+                                   2: its bulk list was sorted by the cost hints (schedule_lpt = 3) */
 } chem_stats;
 
 typedef struct chem_ctx chem_ctx;   /* opaque, library-owned */

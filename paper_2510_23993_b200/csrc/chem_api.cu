@@ -462,7 +462,7 @@ static int check_opts(const chem_opts* o)
         (o->method < CHEM_METHOD_RODAS4 || o->method > CHEM_METHOD_ROS4) ||
         !std::isfinite(o->T_min) || !(o->eps_change > 0.0 && o->eps_change <= 1.0) ||
         (o->temperature_mode != 0 && o->temperature_mode != 1) || (o->refill_bulk != 0 && o->refill_bulk != 1) ||
-        o->lockstep < 0 || o->lockstep > 2 || o->kmax_first < 0 || o->lockstep_sparse < 0 || o->lockstep_sparse > 1 || o->schedule_lpt < 0 || o->schedule_lpt > 2 ||
+        o->lockstep < 0 || o->lockstep > 2 || o->kmax_first < 0 || o->lockstep_sparse < 0 || o->lockstep_sparse > 1 || o->schedule_lpt < 0 || o->schedule_lpt > 3 ||
         !(o->h0_factor > 0.0 && o->h0_factor <= 1.0) ||
         (o->lanes_per_cell != 1 && o->lanes_per_cell != 4 && o->lanes_per_cell != 8))
         return CHEM_EINVAL;
@@ -723,9 +723,10 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
         }
     }
 
-    // ---- Heavy-first schedule (chem_opts.schedule_lpt).  When the cost hints say
-    // most of the work sits in heavy cells (> kHeavySteps substeps last call), the round-robin bulk
-    // bursts would start those cells' long chains late and leave them as the tail.  Instead the
+    // ---- Heavy-first schedule (chem_opts.schedule_lpt).  When the cost hints are
+    // skewed (heavy cells, > kHeavySteps substeps last call, carry half the work, or the costs vary),
+    // the round-robin bulk bursts would start the long chains late and leave them as the tail, and
+    // mix short and long cells in one warp.  Instead the
     // index map is sorted by hint, heaviest first (stable LSD radix sort: ties keep gate order), and
     // the whole list runs as one persistent lockstep launch with warp-batched refill: the longest
     // chains start at once and light cells fill the slots that free up (longest-processing-time
@@ -739,20 +740,18 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
     std::memcpy(c->h_sig, sig, sizeof(sig));
     CK(cudaMemcpyAsync(L.stats + S_SIG0, c->h_sig, sizeof(sig), cudaMemcpyHostToDevice, s));
     const uint64_t pred_total = c->h_stats[S_PRED_TOTAL], pred_heavy = c->h_stats[S_PRED_HEAVY];
-    const bool sortable = n_active > 0 && n_active <= (int64_t)0x7fffffff;   // cub's int item count
-    const bool lpt = sortable && !use_grp && o.method != CHEM_METHOD_EXPLICIT &&
-                     (o.schedule_lpt == 1 ||
-                      (o.schedule_lpt == 2 && history && pred_total > 0 && 2 * pred_heavy >= pred_total));
-    st.lpt = lpt;
-    // Without the heavy-first launch, the hints still sort the bulk bursts' list (descending) when the
-    // cells' costs differ (pred max above the mean): warps then hold cells that need similar numbers
-    // of substeps (fewer idle lanes per burst) and heavy cells start first.
     const uint64_t pred_max = c->h_stats[S_PRED_MAX];
-    const bool sort_bulk_ = !lpt && history && sortable && o.schedule_lpt == 2 && !use_grp &&
-                           o.method != CHEM_METHOD_EXPLICIT && pred_total > 0 &&
-                           (double)pred_max * (double)n_active > 1.5 * (double)pred_total;
-    const bool sort_bulk = sort_bulk_;
-    if (sort_bulk) st.lpt = 2;
+    const bool sortable = n_active > 0 && n_active <= (int64_t)0x7fffffff;   // cub's int item count
+    const bool eligible = sortable && !use_grp && o.method != CHEM_METHOD_EXPLICIT;
+    // hints that vary (max above 1.5x the mean) or put half the work in heavy cells
+    const bool skewed = history && pred_total > 0 &&
+                        (2 * pred_heavy >= pred_total ||
+                         (double)pred_max * (double)n_active > 1.5 * (double)pred_total);
+    const bool lpt = eligible && (o.schedule_lpt == 1 || (o.schedule_lpt == 2 && skewed));
+    // schedule_lpt = 3: keep Alg. 3's bulk bursts but sort their list by the hints (descending):
+    // warps then hold cells that need similar numbers of substeps
+    const bool sort_bulk = eligible && !lpt && o.schedule_lpt == 3 && history && pred_total > 0;
+    st.lpt = lpt ? 1 : (sort_bulk ? 2 : 0);
     const uint32_t* cur = ids0;
     int64_t n_cur = n_active;
     uint32_t* nxt = idsA;
