@@ -10,7 +10,11 @@
  *   - T from (e, Y) by Newton-Raphson at constant (e, rho), |dT| < 1e-13 T;
  *   - a dense variable-order (1..5) variable-step BDF integrator in the quasi-constant
  *     step-size backward-difference form of Shampine & Reichelt, "The MATLAB ODE suite",
- *     SIAM J. Sci. Comput. 18 (1997) (kappa = 0, i.e. plain BDF), simplified Newton with a
+ *     SIAM J. Sci. Comput. 18 (1997) (kappa = 0, i.e. plain BDF) — a C transliteration of
+ *     scipy's scipy/integrate/_ivp/bdf.py (compute_R, change_D, the Newton rate test of
+ *     solve_bdf_system, NEWTON_MAXITER = 4, MIN/MAX_FACTOR, the safety factor and the
+ *     order selection), so the scipy-BDF pin in the tests is a transliteration check and the
+ *     scipy-Radau pin is the independent one — simplified Newton with a
  *     dense Jacobian from complex-step differentiation of the loop RHS, dense LU with
  *     partial pivoting, RMS error norm, landing exactly on t_final;
  *   - reported T_out = Newton(e, Y_out) (SURVEY reading 3).
@@ -256,7 +260,8 @@ static int bdf_integrate(bdf_prob* P, double* y, double tf)
     double J[OR_MAXN * OR_MAXN], LU[OR_MAXN * OR_MAXN];
     int piv[OR_MAXN];
     double t = 0.0;
-    if (tf <= 0.0) return 0;
+    if (!(tf >= 0.0) || isinf(tf)) return -5;    /* negative, NaN or infinite interval: an error */
+    if (tf == 0.0) return 0;
 
     fun(P, y, f0);
     /* initial step (Hairer-Norsett-Wanner I, II.4; scipy select_initial_step with order 1) */

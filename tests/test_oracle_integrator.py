@@ -181,3 +181,28 @@ def test_ignition_delay_trends(oracle_h2):
     r2 = 1 - np.sum((yv - A @ coef) ** 2) / np.sum((yv - yv.mean()) ** 2)
     assert r2 > 0.9
     assert coef[0] > 0          # Arrhenius: tau grows with 1/T
+
+
+def test_ignition_helper_refuses_non_igniting_mixture(oracle_h2):
+    """a mixture with no interior max of dT/dt (cold, 600 K) must raise instead
+    of returning an extrapolated (negative) tau; the BDF refuses a negative interval (rc -5)."""
+    from oracle.ignition import NoIgnition
+    o = oracle_h2
+    m = o.m
+    Y0 = fresh_Y(m)
+    with pytest.raises(NoIgnition):
+        ignition_delay(o, rho_of(m, P_ATM, 600.0, Y0), np.r_[Y0, 600.0], 1e-3, t_max=4e-3)
+    with pytest.raises(RuntimeError, match="rc=-5"):
+        o.integrate_state(rho_of(m, P_ATM, 1200.0, Y0), np.r_[Y0, 1200.0], -1e-7)
+
+
+def test_trajectory_table_is_ignition_trajectories():
+    """data/ (written by tools/make_trajectories.py from the oracle): every stored trajectory has
+    tau > 0 and burns (T rises > 400 K by 2 tau), including the cool jisc shear-layer mixtures."""
+    import synth
+    doc = synth.load_trajectories()
+    for tr in doc["trajectories"]:
+        assert tr["tau"] > 0.0, tr.get("Z")
+        f = np.asarray(tr["t_over_tau"])
+        T = np.asarray(tr["T"])
+        assert T[np.searchsorted(f, 2.0)] - tr["T0"] > 400.0, (tr["kind"], tr.get("Z"))

@@ -26,8 +26,12 @@ FRACS = np.linspace(0.0, 3.0, 241)          # t / tau samples
 
 def _traj(o, rho, Y0, T0, t_end_guess, **meta):
     y0 = np.r_[Y0, T0]
-    tau = ignition_delay(o, rho, y0, t_end_guess)
+    tau = ignition_delay(o, rho, y0, t_end_guess)      # raises NoIgnition if there is none
     ys = trajectory(o, rho, y0, FRACS * tau, **TOL)
+    # the stored states must be an ignition trajectory: tau > 0, T rises through the window
+    assert tau > 0.0, (meta, tau)
+    assert ys[-1, -1] - T0 > 400.0, (meta, T0, ys[-1, -1])
+    assert ys[FRACS.searchsorted(2.0), -1] - T0 > 400.0, (meta, "not burnt by 2 tau")
     return dict(meta, rho=float(rho), tau=float(tau), T0=float(T0), t_over_tau=FRACS.tolist(),
                 T=ys[:, -1].tolist(), Y=ys[:, :-1].tolist())
 
