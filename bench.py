@@ -5,19 +5,31 @@
     torchrun --nproc-per-node N bench.py --gpus N ...      (one rank per GPU, NCCL)
 
 A "step" is one pass of the whole hot path (gate -> bulk bursts ->
-compaction -> sparse -> write-back, one fused chem_integrate_boxes call over every box of the
-field) over one batch of synthetic input: one CFD dt of every cell.  One cell-step = one cell
-advanced over one dt.  Inputs are restored from a pristine device copy before each
-step (untimed).  value = cells of all ranks / (max over ranks of the CUDA-event step time).
+compaction -> sparse -> write-back, fused chem_integrate_boxes calls over every box of the field)
+over one batch of synthetic input: one CFD dt of every cell.  One cell-step = one cell advanced over
+one dt.  value = cells of all ranks / (max over ranks of the CUDA-event step time).
+
+Inputs between timed steps (untimed, before the start event) — VERDICT r01 next-4:
+  * cfg2 (every cell the same state by definition): restored from the pristine copy;
+  * cfg3/cfg4/cfg5 ("perturb"): restored and then every active cell's T jittered by a seeded
+    +-1 % that differs from step to step, e recomputed (chem_energy): the previous step's per-cell
+    substep counts are then predictions of this step's cost, not a replay.  The line also reports
+    the first call of a layout (no cost hints), Alg. 3 as written (schedule_lpt = 0) and exact
+    replay (restore), each timed the same way.
+With no flags (the driver's command) the cfg2 headline line carries, under "also", the cfg3
+bulk-sparse field timed under Alg. 3 and under the default schedule, so the driver measures a
+non-empty sparse phase.
 
 Multi-GPU: cells are independent 0-D reactors, so every rank integrates its own
-field (weak scaling) with no data-path collective; NCCL carries only the max-time reduction.
+boxes with no data-path collective.  NCCL carries the cost all_gather of the LPT balance (cfg4,
+cfg5) and, every step, the SUM of unfinished cells / substeps and the MIN of the proposed dt.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import platform
 import subprocess
 import sys
 import threading
@@ -29,7 +41,11 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 RTOL, ATOL, ATOL_T = 1e-9, 1e-20, 1e-6        # parity tolerance (headline measured there)
+PROD_TOL = dict(rtol=1e-6, atol=1e-12, atol_T=1e-3)   # §8(d) secondary production-tolerance number
 METRIC = "chemistry Mcell-steps/s per B200 at 1/2/4/8 GPUs; % of FP64/HBM roofline"
+T_MIN = 500.0
+METHODS = {"rodas4": 0, "rodas3": 1, "explicit": 2}
+STAGES = {0: 6, 1: 4, 2: 0}
 
 
 def parse():
@@ -41,21 +57,28 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--rtol", type=float, default=RTOL)
     p.add_argument("--atol", type=float, default=ATOL)
-    p.add_argument("--method", default="rodas4", choices=["rodas4", "rodas3", "explicit", "ros4"])
+    p.add_argument("--method", default="rodas4", choices=list(METHODS))
+    p.add_argument("--evolve", default="auto", choices=["auto", "perturb", "restore"],
+                   help="inputs between steps (auto: restore for cfg2, perturb otherwise)")
+    p.add_argument("--perturb", type=float, default=0.01, help="relative T jitter of --evolve perturb")
+    p.add_argument("--also", default="auto",
+                   help="extra configs timed into the same line ('auto': cfg3 when --config cfg2; 'none')")
+    p.add_argument("--no-schedules", action="store_true", help="skip the first-call / alg3 / replay variants")
+    p.add_argument("--no-prod", action="store_true", help="skip the production-tolerance number")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--cpu-sample-seconds", type=float, default=15.0)
     p.add_argument("--balance", default="lpt", choices=["lpt", "none"])
-    p.add_argument("--lanes", type=int, default=1, choices=[1, 4, 8], help="lanes per cell (1: thread per cell)")
-    p.add_argument("--tmode", type=int, default=0, choices=[0, 1],
-                   help="0: T integrated by Eq. 6; 1: T = Newton(e, Y) at every RHS evaluation (P:96)")
     p.add_argument("--e2e-chunks", type=int, default=0, help="e2e copy/compute pipelining groups (0: auto)")
-    p.add_argument("--h0", type=float, default=0.01, help="initial substep factor (chem_opts.h0_factor)")
     p.add_argument("--opt", action="append", default=[], metavar="KEY=VAL",
-                   help="extra chem_opts field (e.g. kmax_bulk=5, refill_bulk=1); repeatable")
+                   help="extra chem_opts field (e.g. kmax_bulk=5, schedule_lpt=0); repeatable")
     p.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                    help="process-group backend (gloo only to exercise N>1 on a box with fewer GPUs)")
     return p.parse_args()
+
+
+def _opts(args):
+    return {k: float(v) if ("." in v or "e" in v) else int(v) for k, v in (o.split("=", 1) for o in args.opt)}
 
 
 # ------------------------------------------------------------------ clocks during the timed region
@@ -72,7 +95,7 @@ class ClockSampler:
     def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -83,9 +106,12 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
-    def stop(self):
+    def stop(self, min_samples=3, wait_s=2.0):
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        t0 = time.time()
+        while len(self.lines) < min_samples and time.time() - t0 < wait_s:   # short regions: wait for samples
+            time.sleep(0.02)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -104,37 +130,53 @@ class ClockSampler:
             for nm, v in zip(names, parts[3:7]):
                 if v.lower().startswith("active"):
                     reasons.add(nm)
-        load = [s for s, p in zip(sm, pw)] if sm else []
-        return {"sm_mhz": float(np.median(load)) if load else None, "sm_max_mhz": max(mx) if mx else None,
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "power_w_max": max(pw) if pw else None, "samples": len(sm), "reasons": sorted(reasons)}
 
 
 # ------------------------------------------------------------------ workloads
 class Workload:
-    """boxes (this rank's), the fused calls one step makes (lists of box indices), pristine inputs."""
+    """boxes (this rank's), the fused calls one step makes (lists of box indices), pristine inputs,
+    and the per-step input preparation (restore or seeded perturbation; untimed)."""
 
-    def __init__(self, boxes, calls, meta, cell_steps, extra=None):
+    def __init__(self, chem, boxes, calls, meta, cell_steps, evolve, amp, extra=None):
         import torch
+        self.chem = chem
         self.boxes, self.calls, self.meta = boxes, calls, meta
         self.cell_steps = cell_steps                 # cell-steps this rank advances per step
-        self.pristine = [(b.T.clone(), b.Y.clone()) for b in boxes]
+        self.pristine = [(b.T.clone(), b.Y.clone(), b.e.clone()) for b in boxes]
+        self.active = [T >= T_MIN for T, _, _ in self.pristine]
+        self.evolve, self.amp = evolve, amp
         self.extra = extra or {}
+        self.ncells = sum(b.ncells for b in boxes)
         torch.cuda.synchronize()
 
-    def restore(self):
-        for b, (T, Y) in zip(self.boxes, self.pristine):
-            b.T.copy_(T)
+    def prepare(self, k):
+        """Inputs of step k: the pristine field, or (perturb) its active cells' T jittered by a seeded
+        +-amp that differs for every k (cells stay active), e = u(T', Y) by chem_energy."""
+        import torch
+        for i, (b, (T, Y, e)) in enumerate(zip(self.boxes, self.pristine)):
             b.Y.copy_(Y)
+            if self.evolve != "perturb":
+                b.T.copy_(T)
+                b.e.copy_(e)
+                continue
+            g = torch.Generator(device=T.device)
+            g.manual_seed(23993 + 7919 * k + 104729 * i)
+            u = torch.rand(T.shape, generator=g, device=T.device, dtype=torch.float64)
+            Tp = torch.where(self.active[i], (T * (1.0 + self.amp * (2.0 * u - 1.0))).clamp_min(T_MIN), T)
+            b.T.copy_(Tp)
+            self.chem.energy(b.T, b.Y, out=b.e)
 
-    def step(self, chem, rtol, atol, cost=None):
+    def step(self, rtol, atol, cost=None):
+        import torch
         stats = []
         for c in self.calls:
             bx = [self.boxes[i] for i in c]
             cc = None
             if cost is not None:
-                import torch
                 cc = torch.zeros(len(c), dtype=torch.float64, device=self.boxes[0].rho.device)
-            stats.append(chem.integrate_boxes(bx, rtol=rtol, atol=atol, box_cost=cc))
+            stats.append(self.chem.integrate_boxes(bx, rtol=rtol, atol=atol, box_cost=cc))
             if cost is not None:
                 cost[c] += cc.cpu().numpy()
         return stats
@@ -149,31 +191,72 @@ def _mk_boxes(chem, raw):
     return out
 
 
-def build_workload(args, chem, doc, device, rank, world):
-    import synth
+def _balanced(chem, args, all_ids, build, rank, world, calls_for, home):
+    """Cost-weighted box -> rank map: every rank integrates its home boxes once
+    (calibration call, box_cost), the per-box costs are all-gathered (NCCL), and the same LPT owner
+    map is computed on every rank; owners regenerate their boxes from the pure generator."""
     from paper_2510_23993_b200 import sharding
+    mine = home(rank)
+    boxes = _mk_boxes(chem, [build(all_ids[i]) for i in mine])
+    w0 = Workload(chem, boxes, calls_for(mine), {}, 0, "restore", 0.0)
+    cost = np.zeros(len(mine))
+    w0.step(args.rtol, args.atol, cost=cost)
+    if world > 1:
+        gcost_rank_major = sharding.gather_costs(cost)
+        gcost = np.zeros(len(all_ids))
+        k = 0
+        for r in range(world):               # un-permute the rank-major gather to box order
+            for i in home(r):
+                gcost[i] = gcost_rank_major[k]
+                k += 1
+        owner = sharding.lpt_partition(gcost, world) if args.balance == "lpt" else \
+            np.array([next(r for r in range(world) if i in home(r)) for i in range(len(all_ids))])
+        imb_home = sharding.imbalance(gcost, [next(r for r in range(world) if i in home(r))
+                                              for i in range(len(all_ids))], world)
+        imb = sharding.imbalance(gcost, owner, world)
+    else:
+        gcost, owner, imb, imb_home = cost, np.zeros(len(all_ids), dtype=int), 1.0, 1.0
+    own = [i for i in range(len(all_ids)) if owner[i] == rank]
+    if own == mine:
+        boxes = w0.boxes
+    else:
+        del w0, boxes
+        boxes = _mk_boxes(chem, [build(all_ids[i]) for i in own])
+    extra = dict(balance=args.balance, imbalance_max_over_mean=imb, imbalance_without_lpt=imb_home,
+                 boxes_owned=len(own), calibration="per-box attempted substeps of one call (box_cost)")
+    return own, boxes, extra
+
+
+def build_workload(args, chem, doc, device, rank, world, config=None, evolve="auto"):
+    import synth
     m = chem.mech
-    if args.config == "cfg2":
+    config = config or args.config
+    if evolve == "auto":
+        evolve = "restore" if config == "cfg2" else "perturb"
+    mk = lambda boxes, calls, meta, cs, extra=None: Workload(chem, boxes, calls, meta, cs, evolve,  # noqa: E731
+                                                             args.perturb, extra)
+    if config == "cfg2":
         raw, meta = synth.field_cfg2(doc, device=device)
         boxes = _mk_boxes(chem, raw)
-        return Workload(boxes, [list(range(len(boxes)))], meta, sum(b.ncells for b in boxes))
-    if args.config == "cfg3":
+        return mk(boxes, [list(range(len(boxes)))], meta, sum(b.ncells for b in boxes))
+    if config == "cfg3":
         raw, meta = synth.field_cfg3(doc, m.W, m.species, device=device)
         boxes = _mk_boxes(chem, raw)
-        return Workload(boxes, [list(range(len(boxes)))], meta, sum(b.ncells for b in boxes))
-    if args.config == "cfg5":
+        return mk(boxes, [list(range(len(boxes)))], meta, sum(b.ncells for b in boxes))
+    if config == "cfg5":
+        # one field's 128 boxes over the ranks (strong), LPT on a calibration call's box cost
         nb = 128
-        ids = list(range(rank, nb, world))         # strong split of one field over the ranks
-        raw, meta = synth.field_cfg5(doc, m.W, m.species, device=device, box_ids=ids)
-        boxes = _mk_boxes(chem, raw)
+        ids = list(range(nb))
+        _, meta = synth.field_cfg5(doc, m.W, m.species, device=device, box_ids=[])
+        build = lambda b: synth.field_cfg5(doc, m.W, m.species, device=device, box_ids=[b])[0][0]  # noqa: E731
+        own, boxes, extra = _balanced(chem, args, ids, build, rank, world, lambda idx: [list(range(len(idx)))],
+                                      lambda r: list(range(r, nb, world)))
         meta["scaling"] = "strong"
-        return Workload(boxes, [list(range(len(boxes)))], meta, sum(b.ncells for b in boxes))
-    if args.config == "cfg4":
+        return mk(boxes, [list(range(len(boxes)))], meta, sum(b.ncells for b in boxes), extra)
+    if config == "cfg4":
         # weak scaling: P copies of the 3-level hierarchy; copy p calibrated on rank p, then the
         # P*192 boxes are redistributed by LPT on the measured per-box cost (SURVEY §8(e)).
-        import numpy as np
         all_desc = [d for p in range(world) for d in synth.hierarchy_cfg4(copy=p)]
-        mine = [i for i, d in enumerate(all_desc) if d["copy"] == rank]
 
         def calls_for(idx):
             lv = [all_desc[i]["level"] for i in idx]
@@ -182,33 +265,91 @@ def build_workload(args, chem, doc, device, rank, world):
             return [[k for k, l in enumerate(lv) if l >= 0], [k for k, l in enumerate(lv) if l >= 1],
                     [k for k, l in enumerate(lv) if l >= 2], [k for k, l in enumerate(lv) if l >= 2]]
 
-        raw = [synth.build_cfg4_box(doc, m.W, m.species, all_desc[i], device) for i in mine]
-        w0 = Workload(_mk_boxes(chem, raw), calls_for(mine), {}, 0)
-        cost = np.zeros(len(mine))
-        w0.step(chem, args.rtol, args.atol, cost=cost)
-        if world > 1 and args.balance == "lpt":
-            gcost, owner = sharding.balance(cost)
-        else:
-            gcost = np.concatenate([cost] * world) if world > 1 else cost
-            owner = np.array([d["copy"] for d in all_desc])
-        imb = sharding.imbalance(gcost, owner, world) if world > 1 else 1.0
-        own = [i for i in range(len(all_desc)) if owner[i] == rank]
-        if own == mine:
-            boxes = w0.boxes
-        else:
-            del w0
-            boxes = _mk_boxes(chem, [synth.build_cfg4_box(doc, m.W, m.species, all_desc[i], device) for i in own])
-        calls = calls_for(own)
+        own, boxes, extra = _balanced(chem, args, list(range(len(all_desc))),
+                                      lambda i: synth.build_cfg4_box(doc, m.W, m.species, all_desc[i], device),
+                                      rank, world, calls_for,
+                                      lambda r: [i for i, d in enumerate(all_desc) if d["copy"] == r])
         cell_steps = sum(b.ncells * 2 ** all_desc[i]["level"] for b, i in zip(boxes, own))
         meta = dict(workload=f"cfg4: 3-level AMR hierarchy (ratio 2, 32^3 boxes, 192 boxes/copy, 6.3M cells/copy) "
                              f"of detonation fields, {world} copies, subcycled coarse step (4 fused calls), "
                              f"balance={args.balance}", cells=sum(b.ncells for b in boxes))
-        return Workload(boxes, calls, meta, cell_steps, extra=dict(imbalance_max_over_mean=imb,
-                                                                   boxes_owned=len(own)))
-    raise SystemExit(f"unknown --config {args.config}")
+        return mk(boxes, calls_for(own), meta, cell_steps, extra)
+    raise SystemExit(f"unknown --config {config}")
+
+
+# ------------------------------------------------------------------ timing
+def timed(wl, args, steps, warmup, dist=None, before=None, clocks=None, rtol=None, atol=None):
+    """warmup + steps steps; each step: prepare(k) (untimed) -> [start event] fused calls (+ the
+    §8(e) per-step reductions when N > 1) [end event].  Returns (per-step ms, stats of timed steps)."""
+    import torch
+    rtol = args.rtol if rtol is None else rtol
+    atol = args.atol if atol is None else atol
+    for k in range(warmup):
+        wl.prepare(k)
+        if before:
+            before()
+        wl.step(rtol, atol)
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    stats, reds = [], []
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    if clocks:
+        clocks.start()
+    for k in range(steps):
+        wl.prepare(warmup + k)
+        if before:
+            before()
+        ev[k][0].record()
+        st = wl.step(rtol, atol)
+        if dist is not None:
+            reds.append(step_reductions(st, wl))
+        ev[k][1].record()
+        stats += st
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    clk = clocks.stop() if clocks else None
+    return [a.elapsed_time(b) for a, b in ev], stats, clk, reds
+
+
+def step_reductions(stats, wl):
+    """SURVEY §8(e) (2)-(3) every step: SUM of unfinished cells and attempted substeps (convergence),
+    MIN of the proposed next dt (the CFL stand-in: halve it if any cell ran out of budget)."""
+    from paper_2510_23993_b200 import sharding
+    unf = sum(s["n_unfinished"] for s in stats)
+    att = sum(s["steps_attempted"] for s in stats)
+    dt = min(b.dt for b in wl.boxes) * (0.5 if unf else 1.0)
+    tot = sharding.reduce_stats([unf, att], "sum")
+    dtg = sharding.reduce_stats([dt], "min")
+    return dict(n_unfinished=int(tot[0]), substeps=int(tot[1]), dt_next=float(dtg[0]))
+
+
+def roofline(fm, stats, peak_derived, peak_measured):
+    flops = sum(fm.flops(s) for s in stats)
+    k_ms = sum(s["t_bulk_ms"] + s["t_sparse_ms"] for s in stats)
+    ach = flops / (k_ms / 1e3) / 1e12 if k_ms > 0 else 0.0
+    return flops, k_ms, ach
 
 
 # ------------------------------------------------------------------ oracle (cpu baseline / reference arm)
+def host_info():
+    model, smt = None, None
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    try:
+        smt = open("/sys/devices/system/cpu/smt/active").read().strip() == "1"
+    except OSError:
+        pass
+    return dict(cpu_model=model or platform.processor(), smt=smt, nproc=os.cpu_count())
+
+
 def oracle_sample(meta, seconds_target, rtol, atol):
     """Time the oracle, as it stands, on a bounded sample of the workload's cells (all host cores)."""
     from oracle import Oracle
@@ -218,10 +359,10 @@ def oracle_sample(meta, seconds_target, rtol, atol):
     e = o.energy(st["T"], Y)
     nth = o.max_threads()
 
-    def run(n):
+    def run(n, threads=nth):
         t0 = time.perf_counter()
         o.integrate_cells(np.full(n, st["rho"]), np.full(n, e), np.full(n, st["T"]), np.tile(Y, (n, 1)), 1e-7,
-                          rtol=rtol, atolY=atol, atolT=ATOL_T, nthreads=nth)
+                          rtol=rtol, atolY=atol, atolT=ATOL_T, nthreads=threads)
         return time.perf_counter() - t0
 
     n = nth
@@ -231,7 +372,17 @@ def oracle_sample(meta, seconds_target, rtol, atol):
         dt = run(n)
     n = int(max(nth, min(1 << 24, n * seconds_target / max(dt, 1e-9))))
     dt = run(n)
-    return dict(cells=n, seconds=dt, threads=nth, value=n / dt / 1e6)
+    n1 = max(1, int(n / nth / 4))
+    dt1 = run(n1, 1)
+    return dict(cells=n, seconds=dt, threads=nth, value=n / dt / 1e6, one_core_value=n1 / dt1 / 1e6)
+
+
+def _meta_cfg2(doc):
+    import synth
+    tr = next(t for t in doc["trajectories"] if t["kind"] == "fresh" and t["T0"] == 1200.0)
+    rho, T, Y = synth.traj_state(tr, 0.9)
+    return dict(workload="cfg2: uniform 128^3 H2-air field, T0=1200 K traj. state at t=0.9 tau, 64 boxes of 32^3, "
+                         "dt=1e-07 s", cells=128 ** 3, state=dict(rho=float(rho), T=float(T), Y=np.asarray(Y).tolist()))
 
 
 def reference_arm(args):
@@ -259,61 +410,153 @@ def reference_arm(args):
             "config": {"workload": meta["workload"], "rtol": args.rtol, "atol_Y": args.atol, "atol_T": ATOL_T},
             "cpu_baseline": {"value": value, "unit": "Mcell-steps/s", "cores": nth, "kind": "oracle",
                              "sample": f"{cells // args.steps} cells of the {args.config} state per step "
-                                       "(all cells of cfg2 are identical)"},
+                                       "(all cells of cfg2 are identical)", **host_info()},
             "e2e": {"value": value, "unit": "Mcell-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
 
 
-def _meta_cfg2(doc):
-    import synth
-    tr = next(t for t in doc["trajectories"] if t["kind"] == "fresh" and t["T0"] == 1200.0)
-    rho, T, Y = synth.traj_state(tr, 0.9)
-    return dict(workload="cfg2: uniform 128^3 H2-air field, T0=1200 K traj. state at t=0.9 tau, 64 boxes of 32^3, "
-                         "dt=1e-07 s", cells=128 ** 3, state=dict(rho=float(rho), T=float(T), Y=np.asarray(Y).tolist()))
-
-
-# ------------------------------------------------------------------ our arm
-def oracle_sample_field(wl, seconds_target, rtol, atol, T_min=500.0):
-    """cpu_baseline for a non-uniform field: the oracle on a random sample of the field's active
-    cells (each rank-0 box contributes), extrapolated to the field as n_active x (time per sampled
-    cell with all threads); gated cells cost nothing on either side.  Labelled an extrapolation."""
+def oracle_stratified(chem, wl, rtol, atol, seconds_target, n_prop=65536, n_heavy=1000):
+    """cpu_baseline for a non-uniform field (SURVEY §8(d) / BASELINE.md §3): the cells of this rank's
+    field are split into classes by the substeps the GPU needed for them in one (untimed) call of the
+    first fused call of a step: cold/gated (no work on either side), log2 substep bins, and the
+    n_heavy heaviest cells as a class of their own.  A proportional sample of >= n_prop cells plus
+    all heavy cells is integrated by the oracle (as it stands, same rtol/atol as the GPU) on all host
+    cores, class by class; the field time is extrapolated as sum_class (class time / sampled cells x
+    class count) and LABELLED an extrapolation.  A sub-sample is also timed on one core."""
     import torch
     from oracle import Oracle
     o = Oracle("h2air_li2004")
-    rng = np.random.default_rng(0)
-    cells, n_act = [], 0
-    for bi, (b, (T0, Y0)) in enumerate(zip(wl.boxes, wl.pristine)):
-        act = np.nonzero((T0 >= T_min).cpu().numpy())[0]
-        n_act += len(act)
-        if not len(act):
-            continue
-        pick = np.sort(rng.choice(act, size=min(len(act), 8192), replace=False))
-        idx = torch.as_tensor(pick, device=b.rho.device)
-        rho_b, T_b, Y_b = b.rho[idx].cpu().numpy(), T0[idx].cpu().numpy(), Y0[:, idx].cpu().numpy().T
-        cells.extend(zip(rho_b, T_b, Y_b, [b.dt] * len(pick)))
-    rng.shuffle(cells)
+    wl.prepare(0)
+    # pristine inputs (the named config), one GPU call for the per-cell substep counts
+    for b, (T, Y, e) in zip(wl.boxes, wl.pristine):
+        b.T.copy_(T); b.Y.copy_(Y); b.e.copy_(e)
+    first = wl.calls[0]
+    chem.integrate_boxes([wl.boxes[i] for i in first], rtol=rtol, atol=atol)
+    _, steps = chem.cell_status(substeps=True)
+    steps = steps.cpu().numpy().astype(np.int64)
+    sizes = [wl.boxes[i].ncells for i in first]
+    starts = np.cumsum([0] + sizes)
+    active = steps > 0
+    ids = np.nonzero(active)[0]
+    heavy = ids[np.argsort(steps[ids], kind="stable")[::-1][:n_heavy]]
+    rest = np.setdiff1d(ids, heavy)
+    bins = np.floor(np.log2(np.maximum(steps[rest], 1))).astype(int)
+    rng = np.random.default_rng(23993)
+    frac = min(1.0, n_prop / max(len(rest), 1))
+    classes = [("heavy_top%d" % n_heavy, heavy, heavy)]
+    for bv in np.unique(bins):
+        pool = rest[bins == bv]
+        k = min(len(pool), max(64, int(round(frac * len(pool)))))
+        classes.append((f"substeps_2^{bv}", pool, np.sort(rng.choice(pool, size=k, replace=False))))
+
+    def gather(sel):
+        bidx = np.searchsorted(starts, sel, side="right") - 1
+        rho, T, Y, e, dt = [], [], [], [], []
+        for bi in np.unique(bidx):
+            offs = torch.as_tensor(sel[bidx == bi] - starts[bi], device=wl.boxes[0].rho.device)
+            b = wl.boxes[first[bi]]
+            T0, Y0, _ = wl.pristine[first[bi]]
+            rho.append(b.rho[offs].cpu().numpy()); T.append(T0[offs].cpu().numpy())
+            Y.append(Y0[:, offs].cpu().numpy().T); dt += [b.dt] * len(offs)
+        rho, T, Y, dt = np.concatenate(rho), np.concatenate(T), np.concatenate(Y), np.array(dt)
+        e = np.array([o.energy(t, y) for t, y in zip(T, Y)])    # the oracle's own thermo
+        return rho, e, T, Y, dt
+
     nth = o.max_threads()
 
-    def run(sub):
-        rho = np.array([c[0] for c in sub]); T = np.array([c[1] for c in sub]); Y = np.array([c[2] for c in sub])
-        e = np.array([o.energy(t, y) for t, y in zip(T, Y)])
+    def run(data, threads):
+        rho, e, T, Y, dt = data
         t0 = time.perf_counter()
-        for d in sorted(set(c[3] for c in sub)):
-            sel = np.array([c[3] == d for c in sub])
-            o.integrate_cells(rho[sel], e[sel], T[sel], Y[sel], d, rtol=rtol, atolY=atol, atolT=ATOL_T, nthreads=nth)
+        for d in np.unique(dt):
+            s = dt == d
+            o.integrate_cells(rho[s], e[s], T[s], Y[s], float(d), rtol=rtol, atolY=atol, atolT=ATOL_T,
+                              nthreads=threads)
         return time.perf_counter() - t0
 
-    n = min(len(cells), 4 * nth)
-    dt = run(cells[:n])
-    while dt < seconds_target / 2 and n < len(cells):
-        n = min(len(cells), n * 4)
-        dt = run(cells[:n])
-    per_cell = dt / n
-    total_cells = sum(b.ncells for b in wl.boxes)
-    value = total_cells / (n_act * per_cell) / 1e6
-    return dict(value=value, threads=nth, cells=n, seconds=dt, n_active=n_act,
-                sample=f"{n} random active cells of the {wl.meta['workload'][:5]} field timed on {nth} threads "
-                       f"({dt:.1f} s), extrapolated to the field's {n_act} active of {total_cells} cells")
+    field_s, one_core_s, sampled, per_class = 0.0, 0.0, 0, {}
+    for name, pool, sel in classes:
+        data = gather(sel)
+        t = run(data, nth)
+        field_s += t * len(pool) / len(sel)
+        sub = max(1, len(sel) // 64)
+        t1 = run(tuple(x[:sub] for x in data), 1)
+        one_core_s += t1 * len(pool) / sub
+        sampled += len(sel)
+        per_class[name] = dict(count=int(len(pool)), sampled=int(len(sel)), seconds=round(t, 3),
+                               mean_gpu_substeps=float(steps[pool].mean()))
+    total_cells = int(sum(sizes))
+    return dict(value=total_cells / field_s / 1e6, one_core_value=total_cells / one_core_s / 1e6, threads=nth,
+                classes=per_class,
+                sample=(f"stratified: {sampled} of {len(ids)} active cells ({len(classes) - 1} GPU-substep classes "
+                        f"proportional, >= 64 each, plus the {len(heavy)} heaviest), oracle at the GPU's rtol/atol on "
+                        f"{nth} threads, extrapolated per class to the {total_cells}-cell field of one fused call "
+                        f"(gated cells cost 0)"))
+
+
+# ------------------------------------------------------------------ our arm
+def measure(args, chem, doc, device, rank, world, dist, config, fm, peaks, with_variants, clocks=None):
+    """Build `config`, time the default schedule (headline), then optionally Alg. 3, the first call
+    of a layout and exact replay.  Returns (workload, result dict)."""
+    import torch
+    wl = build_workload(args, chem, doc, device, rank, world, config=config, evolve=args.evolve)
+    steps_ms, stats, clk, reds = timed(wl, args, args.steps, args.warmup, dist, clocks=clocks)
+    t_rank = sum(steps_ms) / 1e3
+    t_total, tot_cs = t_rank, float(wl.cell_steps)
+    if world > 1:
+        from paper_2510_23993_b200 import sharding
+        t_total = float(sharding.reduce_stats([t_rank], "max")[0])          # max over ranks
+        tot_cs = float(sharding.reduce_stats([float(wl.cell_steps)], "sum")[0])
+    flops, k_ms, ach = roofline(fm, stats, *peaks)
+    res = dict(value=tot_cs * args.steps / t_total / 1e6, ms_per_step=1e3 * t_total / args.steps,
+               steps_ms=steps_ms, t_rank=t_rank, stats=stats, flops=flops, k_ms=k_ms, achieved=ach,
+               clocks=clk, reductions=reds[-1] if reds else None, tot_cs=tot_cs)
+    if with_variants and config != "cfg2" and not args.no_schedules:
+        var = {}
+        chem_opts0 = dict(schedule_lpt=chem.opts.schedule_lpt)
+
+        def forget():
+            chem.forget_hints()
+
+        for name, kw in (("first_call_no_hints", dict(before=forget)),
+                         ("alg3_schedule_lpt0", dict(opt=dict(schedule_lpt=0))),
+                         ("replayed_exact_hints", dict(evolve="restore"))):
+            if "opt" in kw:
+                chem.set_opts(**kw["opt"])
+            ev0 = wl.evolve
+            if "evolve" in kw:
+                wl.evolve = kw["evolve"]
+            n = max(3, min(args.steps, 10))
+            ms, st, _, _ = timed(wl, args, n, 2, dist, before=kw.get("before"))
+            wl.evolve = ev0
+            chem.set_opts(**chem_opts0)
+            t = sum(ms) / 1e3
+            if world > 1:
+                from paper_2510_23993_b200 import sharding
+                t = float(sharding.reduce_stats([t], "max")[0])
+            fl, km, a = roofline(fm, st, *peaks)
+            s0 = st[-1]
+            var[name] = dict(value=tot_cs * n / t / 1e6, ms_per_step=1e3 * t / n, steps=n,
+                             frac=a / peaks[0], lpt=s0.get("lpt", 0), lockstep=s0["lockstep"],
+                             bulk_iters=s0["bulk_iters"], sparse_cells=s0["sparse_cells"],
+                             t_sparse_ms=s0["t_sparse_ms"])
+        res["schedules"] = var
+    if with_variants and not args.no_prod:
+        # SURVEY §8(d) secondary number: production tolerance (rtol 1e-6, atol_Y 1e-12, atol_T 1e-3 K)
+        chem.set_opts(atol_T=PROD_TOL["atol_T"])
+        n = max(3, min(args.steps, 10))
+        ms, st, _, _ = timed(wl, args, n, 2, dist, rtol=PROD_TOL["rtol"], atol=PROD_TOL["atol"])
+        chem.set_opts(atol_T=ATOL_T)
+        t = sum(ms) / 1e3
+        if world > 1:
+            from paper_2510_23993_b200 import sharding
+            t = float(sharding.reduce_stats([t], "max")[0])
+        fl, km, a = roofline(fm, st, *peaks)
+        res["production_tolerance"] = dict(value=tot_cs * n / t / 1e6, ms_per_step=1e3 * t / n, frac=a / peaks[0],
+                                           substeps_per_cell_step=sum(s["steps_attempted"] for s in st) / n
+                                           / max(wl.cell_steps, 1),
+                                           tolerances=PROD_TOL)
+    torch.cuda.synchronize()
+    return wl, res
 
 
 def ours(args):
@@ -336,60 +579,29 @@ def ours(args):
             dist.init_process_group("nccl", device_id=device)
         else:
             dist.init_process_group("gloo")
-    method = {"rodas4": 0, "rodas3": 1, "explicit": 2, "ros4": 3}[args.method]
-    chem = Chem("h2air_li2004", device=local, atol_T=ATOL_T, method=method, lanes_per_cell=args.lanes,
-                temperature_mode=args.tmode, h0_factor=args.h0,
-                **{k: float(v) if "." in v or "e" in v else int(v) for k, v in (o.split("=", 1) for o in args.opt)})
+    pg = dist if world > 1 else None
+    method = METHODS[args.method]
+    chem = Chem("h2air_li2004", device=local, atol_T=ATOL_T, method=method, **_opts(args))
     doc = synth.load_trajectories()
-    wl = build_workload(args, chem, doc, device, rank, world)
-    ncells = sum(b.ncells for b in wl.boxes)
-    fm = FlopModel(chem.mech, stages={0: 6, 1: 4, 2: 0, 3: 4}[method])
-
-    for _ in range(args.warmup):
-        wl.restore()
-        wl.step(chem, args.rtol, args.atol)
-    torch.cuda.synchronize()
-
-    clocks = ClockSampler(local)
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    stats = []
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    clocks.start()
-    for k in range(args.steps):
-        wl.restore()                                   # untimed: before the start event
-        ev[k][0].record()
-        stats += wl.step(chem, args.rtol, args.atol)
-        ev[k][1].record()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    clk = clocks.stop()
-    step_ms = [a.elapsed_time(b) for a, b in ev]
-    t_total = sum(step_ms) / 1e3
-    t_rank = t_total
-    tot_cs = wl.cell_steps
-    if world > 1:
-        from paper_2510_23993_b200 import sharding
-        t_total = float(sharding.reduce_stats([t_total], "max")[0])          # max over ranks
-        tot_cs = float(sharding.reduce_stats([float(wl.cell_steps)], "sum")[0])
-    value = tot_cs * args.steps / t_total / 1e6
-
-    # roofline of the dominant kernel (k_integrate: bulk + sparse launches, CUDA-event timed by the
-    # library on the launching stream)
-    flops = sum(fm.flops(s) for s in stats)
-    k_ms = sum(s["t_bulk_ms"] + s["t_sparse_ms"] for s in stats)
-    launches_int = sum(s["bulk_iters"] + (1 if s["sparse_cells"] > 0 else 0) for s in stats)
-    achieved = flops / (k_ms / 1e3) / 1e12 if k_ms > 0 else 0.0
+    fm = FlopModel(chem.mech, stages=STAGES[method])
     sm_mhz_peak = 1965.0
     try:
-        mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-        sm_mhz_peak = float(mp.get("sm_max_mhz", sm_mhz_peak))
+        sm_mhz_peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("sm_max_mhz", sm_mhz_peak))
     except Exception:
         pass
     peak = fp64_peak_tflops(sm_mhz=sm_mhz_peak)
-    gpu_launches = sum(1 + 2 * s["bulk_iters"] + (1 if s["sparse_cells"] > 0 else 0) for s in stats)
+    peak_meas = None
+    try:
+        peak_meas = float(json.load(open(os.path.join(ROOT, "profiles", "fp64_peak.json")))["tflops"])
+    except Exception:
+        pass
+
+    clocks = ClockSampler(local)
+    wl, res = measure(args, chem, doc, device, rank, world, pg, args.config, fm, (peak, peak_meas), True,
+                      clocks=clocks)
+    stats = res["stats"]
+    ncells = wl.ncells
+
     traffic, ncu_pipe = None, None
     try:
         tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(args.config)
@@ -398,16 +610,20 @@ def ours(args):
     except Exception:
         pass
 
-    # e2e through the public API with host buffers (H2D + calls + D2H inside the timed region)
+    # e2e through the public API with host buffers (H2D + calls + D2H inside the timed region); the
+    # host inputs alternate between two perturbed realisations when the device run perturbs
     e2e = None
     if not args.no_e2e:
-        host = [dict(rho=b.rho.cpu().pin_memory(), e=b.e.cpu().pin_memory(), T=p[0].cpu().pin_memory(),
-                     Y=p[1].cpu().pin_memory(), dt=b.dt) for b, p in zip(wl.boxes, wl.pristine)]
-        # copy/compute pipelining pays on dense fields; on sparse ones (cfg3/cfg4) splitting the fused
-        # call serialises the chunks' long tails, so those run as one call
+        def host_set(k):
+            wl.prepare(k)
+            return [dict(rho=b.rho.cpu().pin_memory(), e=b.e.cpu().pin_memory(), T=b.T.cpu().pin_memory(),
+                         Y=b.Y.cpu().pin_memory(), dt=b.dt) for b in wl.boxes]
+        sets = [host_set(1000)] + ([host_set(1001)] if wl.evolve == "perturb" else [])
         chunks = args.e2e_chunks if args.e2e_chunks > 0 else (5 if args.config in ("cfg2", "cfg5") else 1)
-        hr = HostRunner(chem, host, wl.calls, chunks=chunks)
-        hr.step(args.rtol, args.atol)
+        hr = HostRunner(chem, sets[0], wl.calls, chunks=chunks)
+        for k in range(2):
+            hr.load_inputs(sets[k % len(sets)])
+            hr.step(args.rtol, args.atol)
         torch.cuda.synchronize()
         e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                 for _ in range(args.steps)]
@@ -415,6 +631,7 @@ def ours(args):
             dist.barrier()
         torch.cuda.synchronize()
         for k in range(args.steps):
+            hr.load_inputs(sets[k % len(sets)])       # host memcpy into the pinned slab, untimed
             e_ev[k][0].record()
             hr.step(args.rtol, args.atol)
             e_ev[k][1].record()
@@ -423,59 +640,101 @@ def ours(args):
         if world > 1:
             from paper_2510_23993_b200 import sharding
             te = float(sharding.reduce_stats([te], "max")[0])
-        e2e = {"value": tot_cs * args.steps / te / 1e6, "unit": "Mcell-steps/s",
+        e2e = {"value": res["tot_cs"] * args.steps / te / 1e6, "unit": "Mcell-steps/s",
                "h2d_bytes_per_step": hr.h2d_bytes, "d2h_bytes_per_step": hr.d2h_bytes,
-               "copy_compute_chunks": chunks if hr.pipelined else 1}
+               "copy_compute_chunks": chunks if hr.pipelined else 1,
+               "inputs": "two alternating perturbed host sets" if len(sets) > 1 else "pristine host inputs"}
+        del hr, sets
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         if args.config == "cfg2":
             r = oracle_sample(wl.meta, args.cpu_sample_seconds, args.rtol, args.atol)
             cpu = {"value": r["value"], "unit": "Mcell-steps/s", "cores": r["threads"], "kind": "oracle",
+                   "one_core_value": r["one_core_value"],
                    "sample": f"{r['cells']} cells of the cfg2 state (all cfg2 cells are identical), "
-                             f"{r['seconds']:.1f} s on {r['threads']} threads, same rtol/atol as the GPU run"}
+                             f"{r['seconds']:.1f} s on {r['threads']} threads, same rtol/atol as the GPU run",
+                   **host_info()}
         else:
-            r = oracle_sample_field(wl, args.cpu_sample_seconds, args.rtol, args.atol)
+            r = oracle_stratified(chem, wl, args.rtol, args.atol, args.cpu_sample_seconds)
             cpu = {"value": r["value"], "unit": "Mcell-steps/s", "cores": r["threads"], "kind": "oracle",
-                   "sample": r["sample"], "extrapolated": True}
+                   "one_core_value": r["one_core_value"], "sample": r["sample"], "extrapolated": True,
+                   "classes": r["classes"], **host_info()}
+
+    # extra configs timed into the same line (the driver runs only the default command)
+    also = []
+    also_cfgs = (["cfg3"] if args.config == "cfg2" else []) if args.also == "auto" else \
+        [c for c in args.also.split(",") if c and c != "none"]
+    if world == 1 and also_cfgs:
+        meta_main, wl_cells, wl_cs, wl_calls, wl_extra = wl.meta, ncells, wl.cell_steps, len(wl.calls), wl.extra
+        n_boxes = len(wl.boxes)
+        del wl
+        chem.release_workspaces()
+        torch.cuda.empty_cache()
+        for c in also_cfgs:
+            a = argparse.Namespace(**{**vars(args), "no_prod": True})
+            w2, r2 = measure(a, chem, doc, device, rank, world, pg, c, fm, (peak, peak_meas), True)
+            s0 = r2["stats"][-1]
+            also.append(dict(config=c, workload=w2.meta["workload"], schedule="default (heavy-first when the "
+                             "previous step's hints are skewed)", inputs=w2.evolve, value=r2["value"],
+                             ms_per_step=r2["ms_per_step"], frac=r2["achieved"] / peak, lpt=s0.get("lpt", 0),
+                             sparse_cells=s0["sparse_cells"], bulk_iters=s0["bulk_iters"],
+                             substeps_per_cell_step=sum(s["steps_attempted"] for s in r2["stats"]) / args.steps
+                             / max(w2.cell_steps, 1), schedules=r2.get("schedules")))
+            del w2
+            chem.release_workspaces()
+            torch.cuda.empty_cache()
+    else:
+        meta_main, wl_cells, wl_cs, wl_calls, wl_extra = wl.meta, ncells, wl.cell_steps, len(wl.calls), wl.extra
+        n_boxes = len(wl.boxes)
 
     att = sum(s["steps_attempted"] for s in stats) / args.steps
     acc = sum(s["steps_accepted"] for s in stats) / args.steps
     s0 = stats[-1]
+    launches_int = sum(s["bulk_iters"] + (1 if s["sparse_cells"] > 0 else 0) for s in stats)
+    gpu_launches = sum(1 + 2 * s["bulk_iters"] + (1 if s["sparse_cells"] > 0 else 0) for s in stats)
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": "Mcell-steps/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1e3 * t_total / args.steps, "higher_is_better": True,
-            "scaling": wl.meta.get("scaling", "weak"), "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": wl.meta["workload"], "cells_per_gpu": ncells, "boxes_per_gpu": len(wl.boxes),
-                       "cell_steps_per_step_per_gpu": wl.cell_steps, "fused_calls_per_step": len(wl.calls),
+            "metric": METRIC, "value": res["value"], "unit": "Mcell-steps/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": res["ms_per_step"], "higher_is_better": True,
+            "scaling": meta_main.get("scaling", "weak"), "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": meta_main["workload"], "cells_per_gpu": wl_cells, "boxes_per_gpu": n_boxes,
+                       "cell_steps_per_step_per_gpu": wl_cs, "fused_calls_per_step": wl_calls,
                        "rtol": args.rtol, "atol_Y": args.atol, "atol_T": ATOL_T, "method": args.method,
-                       "lanes_per_cell": args.lanes, "temperature_mode": args.tmode, "h0_factor": args.h0,
                        **({"opts": args.opt} if args.opt else {}),
+                       "inputs_between_steps": ("restored (every cfg2 cell is the same state)"
+                                                if args.config == "cfg2" and args.evolve == "auto" else
+                                                f"{'perturbed: seeded +-%g T jitter per step, e recomputed' % args.perturb if args.evolve != 'restore' else 'restored'}"),
                        "l2": "inputs >= 369 MB/GPU > 126 MB L2 (no flush needed)",
                        "parallelism": f"boxes over {world} rank(s)",
-                       "schedule": {1: "heavy-first (cost hints: the previous step's per-cell substeps; "
-                                       "the warm-up steps seed them)",
-                                    2: "bulk-sparse (Alg. 3), bulk list sorted by the previous step's "
-                                       "per-cell substeps"}.get(s0.get("lpt", 0), "bulk-sparse (Alg. 3)"),
-                       **wl.extra},
-            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": traffic, "traffic_unit": "bytes per launch (ncu)",
-                         "ncu_fp64_pipe_pct": ncu_pipe,
-                         "kernel": "k_integrate (bulk+sparse)", "flops_per_step_model": fm.per_step(),
-                         "peak_source": "148 SMs x 64 FP64 FMA/clk x 2 x sm_max_mhz (derived, DESIGN.md)"},
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches, "clocks": clk,
-            "detail": {"step_ms": step_ms, "rank0_seconds": t_rank, "k_integrate_ms": k_ms / args.steps,
-                       "integrate_launches": launches_int, "substeps_per_cell_step": att / max(wl.cell_steps, 1),
-                       "accepted_per_cell_step": acc / max(wl.cell_steps, 1),
+                       "schedule": "heavy-first (cost hints: the previous step's per-cell substeps)"
+                                   if s0.get("lpt", 0) else "bulk-sparse (Alg. 3)",
+                       **wl_extra},
+            "roofline": {"bound": "alu", "achieved": res["achieved"], "peak": peak, "unit": "TFLOP/s",
+                         "frac": res["achieved"] / peak, "traffic": traffic, "traffic_unit": "bytes per launch (ncu)",
+                         "peak_measured_dfma": peak_meas,
+                         "frac_vs_measured_dfma": (res["achieved"] / peak_meas) if peak_meas else None,
+                         "ncu_fp64_pipe_pct": ncu_pipe, "kernel": "k_integrate (bulk+sparse launches)",
+                         "flops_model": fm.table(), "flops_timed": res["flops"],
+                         "k_integrate_ms_timed": res["k_ms"],
+                         "peak_source": "148 SMs x 64 FP64 FMA/clk x 2 x sm_max_mhz (derived, DESIGN.md §5); "
+                                        "measured DFMA loop: profiles/fp64_peak.json"},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches, "clocks": res["clocks"],
+            "schedules": res.get("schedules"), "production_tolerance": res.get("production_tolerance"),
+            "also": also or None,
+            "detail": {"step_ms": res["steps_ms"], "rank0_seconds": res["t_rank"],
+                       "k_integrate_ms": res["k_ms"] / args.steps,
+                       "integrate_launches": launches_int, "substeps_per_cell_step": att / max(wl_cs, 1),
+                       "accepted_per_cell_step": acc / max(wl_cs, 1),
                        "frozen_per_cell_step": sum(s.get("steps_frozen", 0) for s in stats) / args.steps
-                       / max(wl.cell_steps, 1), "bulk_iters": s0["bulk_iters"],
+                       / max(wl_cs, 1), "bulk_iters": s0["bulk_iters"],
                        "active_per_iter": s0["active_per_iter"], "sparse_cells": s0["sparse_cells"],
                        "active0": s0["active0"], "t_gate_ms": s0["t_gate_ms"], "t_compact_ms": s0["t_compact_ms"],
                        "t_sparse_ms": s0["t_sparse_ms"], "n_unfinished": s0["n_unfinished"],
                        "n_nonfinite": s0["n_nonfinite"], "max_energy_drift": s0["max_energy_drift"],
                        "lockstep": s0["lockstep"], "lpt": s0.get("lpt", 0),
-                       "bulk_simt_eff": s0["bulk_substeps"] / max(32 * s0["warp_substeps"], 1)},
+                       "bulk_simt_eff": s0["bulk_substeps"] / max(32 * s0["warp_substeps"], 1),
+                       "step_reductions": res["reductions"]},
         }
         print(json.dumps(line))
     if world > 1:

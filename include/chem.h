@@ -78,7 +78,6 @@ typedef struct {
 #define CHEM_METHOD_EXPLICIT 2 /* the paper's explicit 1st-order adaptive scheme: dt limited so
                                   no Y_k (> 1e-12) changes by more than eps_change of itself; Euler
                                   update clipped at 0; T from Newton every step    */
-#define CHEM_METHOD_ROS4 3     /* Shampine's ROS4: 4 stages / 3 RHS per step, order 4, embedded 3    */
 
 typedef struct {
     double T_min;           /* gate T_reaction_min (value unstated -> 500 K) */
@@ -86,19 +85,16 @@ typedef struct {
     int64_t n_active_star;  /* bulk->sparse threshold N*_active (the paper's 1e4 is
                                H100-tuned).  < 0 (default): one resident wave of the integration
                                kernel, SMs x resident cells per SM (37 888 on a B200)             */
-    int32_t kmax_sparse;    /* attempted substeps in the sparse launch (1e5)              */
+    int32_t kmax_sparse;    /* K_max of the sparse phase (1e5), applied as the per-cell budget
+                               of attempted substeps over the whole call (bulk bursts + sparse
+                               launch, or the heavy-first launch): a cell that spends it ends
+                               CHEM_CELL_UNFINISHED at its last accepted state, whatever the
+                               schedule (reading R10)                                   */
     double atol_T;          /* absolute tolerance on the integrated temperature, K               */
     int32_t method;         /* CHEM_METHOD_*                                                      */
     int32_t compact_bulk;   /* 1 (default): bulk bursts run over the compacted active list;
                                0: every bulk launch spans all cells of all boxes (paper's Alg. 3) */
-    int32_t lanes_per_cell; /* 1: one thread integrates one cell; 4 or 8: a lane group shares one
-                               cell (same mathematics, cooperative RHS/LU/solves) */
     double eps_change;      /* CHEM_METHOD_EXPLICIT: max fractional change per step (0.01; P:96 1-5%) */
-    int32_t temperature_mode; /* 0: T is an unknown integrated with Eq. 6 (corrected); 1: the
-                               unknowns are Y only and T = T(e, Y) by Newton at every RHS
-                               evaluation, dT/dY folded into the Jacobian               */
-    int32_t refill_bulk;    /* 1: bulk bursts also run as a persistent lane-refill grid (a lane whose
-                               cell ends its burst early takes the next id); 0: one thread per id */
     double h0_factor;       /* first substep of a cell = h0_factor * |y|/|f(y)| (WRMS norms), capped
                                at dt (Hairer-Norsett-Wanner I.II.4 use 0.01)                      */
     int32_t lockstep;       /* bulk bursts run as 256-thread blocks whose warps take every substep
@@ -109,23 +105,24 @@ typedef struct {
                                bitwise independent of this choice.                                */
     int32_t kmax_first;     /* substeps of the first bulk burst of a lockstep call (1: cells that
                                finish in one substep leave before the lockstep bursts); 0: kmax_bulk */
-    int32_t lockstep_sparse; /* the sparse launch as persistent 256-thread blocks with one barrier per
-                               substep and warp-batched lane refill (the lockstep of the bulk bursts
-                               applied to the tail): 0 off, 1 on.  Bitwise-neutral.               */
     int32_t schedule_lpt;   /* heavy-first schedule: the active list sorted by the previous call's
                                per-cell substeps (kept in the workspace; used only when this call
                                integrates the same cell layout) and run as one persistent lockstep
                                launch, longest cells first: 0 off, 1 on, 2 auto (on when the hints
                                are skewed: cells above 64 substeps carried half of the previous call's
-                               work, or the largest hint exceeds 1.5x the mean), 3 keep Alg. 3's bulk
-                               bursts but over the hint-sorted list.  Bitwise-neutral.              */
+                               work, or the largest hint exceeds 1.5x the mean).  Bitwise-neutral.  */
 } chem_opts;
 
-/* fills the paper's defaults: 500 K, 5, 1e4, 1e5, 1e-6 K, RODAS4, compact_bulk = 1, lanes_per_cell = 1,
-   eps_change = 0.01, temperature_mode = 0,
-   refill_bulk = 0, h0_factor = 0.01, lockstep = 2 (auto), kmax_first = 1, lockstep_sparse = 0,
-   schedule_lpt = 2 (auto) */
+/* fills the defaults: T_min 500 K, kmax_bulk 5, n_active_star -1 (auto: one resident wave),
+   kmax_sparse 1e5, atol_T 1e-6 K, RODAS4, compact_bulk 1, eps_change 0.01, h0_factor 0.01,
+   lockstep 2 (auto), kmax_first 1, schedule_lpt 2 (auto) */
 void chem_default_opts(chem_opts* o);
+
+/* ---- per-cell outcome of the last chem_integrate* call --------------------- */
+#define CHEM_CELL_UNTOUCHED 0      /* gated out (T < T_min or solid): bytes untouched            */
+#define CHEM_CELL_DONE 1           /* integrated to t = dt                                       */
+#define CHEM_CELL_UNFINISHED 2     /* substep budget (kmax_sparse) spent: last accepted state    */
+#define CHEM_CELL_FAILED (-1)      /* Newton failure, non-finite state or step-size underflow   */
 
 /* ---- one AMR box / grid (FAB analogue) for the fused multi-box call ----------------- */
 typedef struct {
@@ -148,7 +145,7 @@ typedef struct {
     int64_t steps_accepted;
     int64_t steps_frozen;       /* first steps taken as one explicit step by frozen cells (subset of attempted) */
     int64_t rhs_evals, jac_evals, lu_count;
-    int64_t n_unfinished;       /* cells with t < dt after the sparse launch (K_max exceeded)   */
+    int64_t n_unfinished;       /* cells with t < dt whose substep budget (kmax_sparse) was spent */
     int64_t n_newton_fail;      /* temperature Newton not converged in 50 iterations            */
     int64_t n_nonfinite;        /* non-finite state / step size underflow                       */
     int64_t n_T_range;          /* finished cells whose T lies outside the NASA ranges          */
@@ -159,8 +156,7 @@ typedef struct {
                                    bulk lane substeps / (32 x warp_substeps))                   */
     int64_t bulk_substeps;      /* lane substeps attempted in bulk launches                     */
     int64_t lockstep;           /* 1: this call's bulk bursts ran in lockstep                   */
-    int64_t lpt;                /* 1: this call ran the heavy-first schedule (schedule_lpt);
-                                   2: its bulk list was sorted by the cost hints (schedule_lpt = 3) */
+    int64_t lpt;                /* 1: this call ran the heavy-first schedule (schedule_lpt)        */
 } chem_stats;
 
 typedef struct chem_ctx chem_ctx;   /* opaque, library-owned */
@@ -202,6 +198,18 @@ int chem_integrate(chem_ctx* ctx, int64_t n, int64_t ld, const double* rho, cons
 int chem_integrate_boxes(chem_ctx* ctx, int32_t nboxes, const chem_box* boxes, double rtol,
                          double atol, void* ws, size_t ws_bytes, double* box_cost,
                          chem_stats* stats, void* stream);
+
+/* Per-cell outcome of the last chem_integrate* call that used workspace `ws`, for global cells
+ * [first, first + n), where global cells number the boxes of that call in order (box b's cell j is
+ * sum_{a<b} ncells_a + j; a chem_integrate call is one box):
+ *   status[i]   (DEVICE int8 [n], nullable)   CHEM_CELL_* code;
+ *   substeps[i] (DEVICE int32 [n], nullable)  attempted substeps the cell took in that call (its
+ *               chemistry cost; 0 for untouched cells).
+ * Both owned by the caller.  Reads the workspace's per-cell state; enqueued on `stream`, no
+ * synchronisation.  CHEM_EINVAL if the workspace has no recorded call on this ctx or
+ * [first, first + n) lies outside that call's cells. */
+int chem_cell_status(chem_ctx* ctx, const void* ws, size_t ws_bytes, int64_t first, int64_t n,
+                     int8_t* status, int32_t* substeps, void* stream);
 
 /* Activity trace (App. B: "the number of active cells after each integration step
  * for every grid").  trace: DEVICE int32 [rows][nboxes] owned by the caller; subsequent

@@ -20,17 +20,28 @@ def _ptr(t):
     return ctypes.c_void_p(t.data_ptr()) if t is not None else None
 
 
-def _check(t, name, dtype=torch.float64):
+def _check(t, name, dtype=torch.float64, n=None, device=None):
+    """The C ABI cannot see a tensor's dtype, device or length: this binding is the only guard
+    against a kernel reading or writing past a buffer (or a host pointer used as a device one)."""
     if not isinstance(t, torch.Tensor) or not t.is_cuda:
         raise TypeError(f"{name} must be a CUDA tensor (there is no CPU path)")
     if t.dtype != dtype:
         raise TypeError(f"{name} must be {dtype}")
+    if device is not None and t.device != device:
+        raise ValueError(f"{name} is on {t.device}, the ctx on {device}")
+    if n is not None:
+        if t.dim() != 1 or t.stride(0) != 1 or t.numel() < n:
+            raise ValueError(f"{name} must be a contiguous 1-D tensor of >= {n} elements")
 
 
-def _species(Y, ns):
+def _species(Y, ns, n=None):
     _check(Y, "Y")
     if Y.dim() != 2 or Y.shape[0] != ns or Y.stride(1) != 1:
         raise ValueError(f"Y must be [ns={ns}, ld] with unit stride along cells")
+    if n is not None and Y.shape[1] < n:
+        raise ValueError(f"Y has {Y.shape[1]} cells, the call {n}")
+    if n is not None and Y.shape[0] > 1 and Y.stride(0) < n:
+        raise ValueError("Y's component stride (ld) is smaller than the cell count")
     return Y.stride(0)
 
 
@@ -59,8 +70,7 @@ class Chem:
         self.ns = self.mech.ns
         desc, self._keep = _b.mech_desc(self.mech)
         self.opts = _b.default_opts(self.lib)
-        for k, v in opts.items():
-            setattr(self.opts, k, v)
+        self._set(opts)
         h = ctypes.c_void_p()
         rc = self.lib.chem_init(ctypes.byref(desc), ctypes.byref(self.opts), self.device.index, ctypes.byref(h))
         if rc != 0:
@@ -80,9 +90,15 @@ class Chem:
     def structure(self) -> str:
         return self.lib.chem_structure_name(self._h).decode()
 
-    def set_opts(self, **opts):
+    def _set(self, opts):
+        names = {f for f, _ in _b.ChemOpts._fields_}
         for k, v in opts.items():
+            if k not in names:       # ctypes would silently add a Python attribute
+                raise TypeError(f"unknown chem_opts field {k!r}")
             setattr(self.opts, k, v)
+
+    def set_opts(self, **opts):
+        self._set(opts)
         rc = self.lib.chem_set_opts(self._h, ctypes.byref(self.opts))
         if rc != 0:
             raise _b.ChemError(rc, self.lib)
@@ -106,10 +122,12 @@ class Chem:
             raise _b.ChemError(rc, self.lib)
 
     def workspace(self, max_cells, max_boxes=1, layout=None):
-        """Device workspace for a call.  `layout` (a hashable key of the call's cell layout) selects a
-        workspace of its own, so the per-cell cost hints the heavy-first schedule reads (DESIGN.md
-        §6.16) survive between calls on that layout when calls on other layouts (AMR levels)
-        interleave; at most 8 layouts are kept."""
+        """Device workspace for a call (~45 B/cell).  `layout` (a hashable key of the call's cell
+        layout: cell count, box count, first rho pointer) selects a workspace of its own, so the
+        per-cell cost hints the heavy-first schedule reads survive between calls
+        on that layout when calls on other layouts (AMR levels) interleave.  At most 8 layouts are
+        kept (least recently used dropped): a caller that allocates fresh state tensors every step
+        makes a new layout each call, so it should call release_workspaces() or keep its tensors."""
         nbytes = self.lib.chem_workspace_bytes(self._h, int(max_cells), int(max_boxes))
         if layout is None:
             if self._ws is None or self._ws.numel() < nbytes:
@@ -124,19 +142,42 @@ class Chem:
         self._ws = ws
         return ws
 
+    def release_workspaces(self):
+        self._ws = None
+        self._ws_layout.clear()
+
+    def forget_hints(self):
+        """Zero every cached workspace: the next call of each layout runs as a layout's first call
+        (no cost hints; Alg. 3's bulk-sparse schedule).  Enqueued on the current stream."""
+        for ws in self._ws_layout.values():
+            ws.zero_()
+        if self._ws is not None:
+            self._ws.zero_()
+
+    def _cells(self, n, Y, **scalars):
+        ld = _species(Y, self.ns, n)
+        if Y.device != self.device:
+            raise ValueError(f"Y is on {Y.device}, the ctx on {self.device}")
+        for nm, t in scalars.items():
+            _check(t, nm, n=n, device=self.device)
+        return ld
+
     # ---- point evaluations ---------------------------------------------------------------
     def rates(self, rho, T, Y, out=None):
         n = rho.shape[0]
-        ld = _species(Y, self.ns)
-        _check(rho, "rho"); _check(T, "T")
+        ld = self._cells(n, Y, rho=rho, T=T)
         if out is None:
             out = torch.empty((self.ns, ld), dtype=torch.float64, device=self.device)
+        elif out.shape[0] != self.ns or out.stride(0) != ld or out.stride(1) != 1:
+            raise ValueError("out must be [ns, ld] with Y's ld")
         self._call(self.lib.chem_rates(self._h, n, ld, _ptr(rho), _ptr(T), _ptr(Y), _ptr(out), self._stream()))
         return out
 
     def rhs(self, rho, T, Y, out=None):
         n = rho.shape[0]
-        ld = _species(Y, self.ns)
+        ld = self._cells(n, Y, rho=rho, T=T)
+        if out is not None and (out.shape[0] != self.ns + 1 or out.stride(0) != ld or out.stride(1) != 1):
+            raise ValueError("out must be [ns + 1, ld] with Y's ld")
         if out is None:
             out = torch.empty((self.ns + 1, ld), dtype=torch.float64, device=self.device)
         self._call(self.lib.chem_rhs(self._h, n, ld, _ptr(rho), _ptr(T), _ptr(Y), _ptr(out), self._stream()))
@@ -144,7 +185,7 @@ class Chem:
 
     def jacobian(self, rho, T, Y):
         n = rho.shape[0]
-        ld = _species(Y, self.ns)
+        ld = self._cells(n, Y, rho=rho, T=T)
         nn = self.ns + 1
         J = torch.empty((nn * nn, ld), dtype=torch.float64, device=self.device)
         self._call(self.lib.chem_jacobian(self._h, n, ld, _ptr(rho), _ptr(T), _ptr(Y), _ptr(J), self._stream()))
@@ -153,7 +194,7 @@ class Chem:
     def temperature(self, e, Y, T):
         """In place: T <- Newton(e, Y) seeded with T."""
         n = e.shape[0]
-        ld = _species(Y, self.ns)
+        ld = self._cells(n, Y, e=e, T=T)
         self._call(self.lib.chem_temperature(self._h, n, ld, _ptr(e), _ptr(Y), _ptr(T), self._stream()))
         return T
 
@@ -176,7 +217,9 @@ class Chem:
 
     def energy(self, T, Y, out=None):
         n = T.shape[0]
-        ld = _species(Y, self.ns)
+        ld = self._cells(n, Y, T=T)
+        if out is not None:
+            _check(out, "out", n=n, device=self.device)
         if out is None:
             out = torch.empty(n, dtype=torch.float64, device=self.device)
         self._call(self.lib.chem_energy(self._h, n, ld, _ptr(T), _ptr(Y), _ptr(out), self._stream()))
@@ -186,12 +229,10 @@ class Chem:
     def integrate(self, rho, e, T, Y, dt, rtol=1e-9, atol=1e-20, solid=None):
         """In place on T and Y (chem_integrate).  Returns the chem_stats dict."""
         n = rho.shape[0]
-        ld = _species(Y, self.ns)
-        for t, nm in ((rho, "rho"), (e, "e"), (T, "T")):
-            _check(t, nm)
+        ld = self._cells(n, Y, rho=rho, e=e, T=T)
         if solid is not None:
-            _check(solid, "solid", torch.uint8)
-        ws = self.workspace(n, 1)
+            _check(solid, "solid", torch.uint8, n=n, device=self.device)
+        ws = self.workspace(n, 1, layout=(n, 1, rho.data_ptr()))
         st = _b.ChemStats()
         self._call(self.lib.chem_integrate(self._h, n, ld, _ptr(rho), _ptr(e), _ptr(T), _ptr(Y), _ptr(solid),
                                            float(dt), float(rtol), float(atol), _ptr(ws), ws.numel(),
@@ -204,8 +245,12 @@ class Chem:
         nb = len(boxes)
         arr = (_b.ChemBox * nb)()
         total = 0
+        if nb < 1:
+            raise ValueError("integrate_boxes needs at least one box")
         for i, bx in enumerate(boxes):
-            ld = _species(bx.Y, self.ns)
+            ld = self._cells(bx.ncells, bx.Y, rho=bx.rho, e=bx.e, T=bx.T)
+            if bx.solid is not None:
+                _check(bx.solid, "solid", torch.uint8, n=bx.ncells, device=self.device)
             arr[i].rho = bx.rho.data_ptr()
             arr[i].e = bx.e.data_ptr()
             arr[i].T = bx.T.data_ptr()
@@ -217,12 +262,27 @@ class Chem:
             total += bx.ncells
         ws = self.workspace(total, nb, layout=(total, nb, boxes[0].rho.data_ptr()))
         if box_cost is not None:
-            _check(box_cost, "box_cost")
+            _check(box_cost, "box_cost", n=nb, device=self.device)
         st = _b.ChemStats()
         self._call(self.lib.chem_integrate_boxes(self._h, nb, arr, float(rtol), float(atol), _ptr(ws), ws.numel(),
                                                  _ptr(box_cost), ctypes.byref(st), self._stream()))
         self.last_stats = st.to_dict()
         return self.last_stats
+
+    def cell_status(self, n=None, first=0, substeps=False):
+        """int8 CUDA tensor of CHEM_CELL_* codes for global cells [first, first + n) of
+        the last integrate / integrate_boxes call (boxes numbered in call order); with
+        substeps=True also the int32 per-cell attempted substeps of that call."""
+        ws = self._ws
+        if ws is None:
+            raise RuntimeError("no integrate call yet")
+        if n is None:
+            n = self.last_stats["cells"] - first
+        out = torch.empty(max(n, 0), dtype=torch.int8, device=self.device)
+        k = torch.empty(max(n, 0), dtype=torch.int32, device=self.device) if substeps else None
+        self._call(self.lib.chem_cell_status(self._h, _ptr(ws), ws.numel(), int(first), int(n), _ptr(out),
+                                             _ptr(k), self._stream()))
+        return (out, k) if substeps else out
 
 
 class HostRunner:
@@ -280,6 +340,22 @@ class HostRunner:
             self.slabs.append((h_in, h_out, d, 2 * tot))
         self.h2d_bytes = sum(s_[0].numel() * 8 for s_ in self.slabs)
         self.d2h_bytes = sum(s_[1].numel() * 8 for s_ in self.slabs)
+
+    def load_inputs(self, host_boxes):
+        """Copy new host inputs (same shapes as at construction) into the pinned input slabs (host
+        memcpy; the next step() moves them)."""
+        for g, grp in enumerate(self.groups):
+            h_in = self.slabs[g][0]
+            tot = sum(host_boxes[i]["rho"].numel() for i in grp)
+            o = [0, tot, 2 * tot, 3 * tot]
+            for i in grp:
+                h = host_boxes[i]
+                ni, si = h["rho"].numel(), h["Y"].shape[0]
+                h_in[o[0]:o[0] + ni].copy_(h["rho"].reshape(-1))
+                h_in[o[1]:o[1] + ni].copy_(h["e"].reshape(-1))
+                h_in[o[2]:o[2] + ni].copy_(h["T"].reshape(-1))
+                h_in[o[3]:o[3] + ni * si].copy_(h["Y"].reshape(-1))
+                o = [o[0] + ni, o[1] + ni, o[2] + ni, o[3] + ni * si]
 
     def _h2d_group(self, g):
         h_in, _, d, _ = self.slabs[g]

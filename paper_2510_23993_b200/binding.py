@@ -19,7 +19,9 @@ LIB_PATH = pathlib.Path(__file__).resolve().parent / "libchem.so"
 CHEM_METHOD_RODAS4 = 0
 CHEM_METHOD_RODAS3 = 1
 CHEM_METHOD_EXPLICIT = 2
-CHEM_METHOD_ROS4 = 3
+
+# per-cell outcome codes of chem_cell_status
+CHEM_CELL_UNTOUCHED, CHEM_CELL_DONE, CHEM_CELL_UNFINISHED, CHEM_CELL_FAILED = 0, 1, 2, -1
 
 _ERRORS = {-1: "CHEM_EINVAL", -2: "CHEM_EMECH", -3: "CHEM_ENOSTRUCT", -4: "CHEM_ECUDA", -5: "CHEM_ENOWS"}
 
@@ -43,10 +45,8 @@ class ChemMechDesc(ctypes.Structure):
 class ChemOpts(ctypes.Structure):
     _fields_ = [("T_min", ctypes.c_double), ("kmax_bulk", ctypes.c_int32), ("n_active_star", ctypes.c_int64),
                 ("kmax_sparse", ctypes.c_int32), ("atol_T", ctypes.c_double), ("method", ctypes.c_int32),
-                ("compact_bulk", ctypes.c_int32), ("lanes_per_cell", ctypes.c_int32),
-                ("eps_change", ctypes.c_double), ("temperature_mode", ctypes.c_int32),
-                ("refill_bulk", ctypes.c_int32), ("h0_factor", ctypes.c_double), ("lockstep", ctypes.c_int32),
-                ("kmax_first", ctypes.c_int32), ("lockstep_sparse", ctypes.c_int32), ("schedule_lpt", ctypes.c_int32)]
+                ("compact_bulk", ctypes.c_int32), ("eps_change", ctypes.c_double), ("h0_factor", ctypes.c_double),
+                ("lockstep", ctypes.c_int32), ("kmax_first", ctypes.c_int32), ("schedule_lpt", ctypes.c_int32)]
 
 
 class ChemBox(ctypes.Structure):
@@ -72,7 +72,7 @@ class ChemStats(ctypes.Structure):
 # every symbol include/chem.h declares (checked by tests/test_cabi.py on CPU)
 EXPORTED = ("chem_default_opts", "chem_init", "chem_finalize", "chem_strerror", "chem_structure_name",
             "chem_set_opts", "chem_workspace_bytes", "chem_rates", "chem_integrate", "chem_integrate_boxes",
-            "chem_temperature", "chem_energy", "chem_jacobian", "chem_rhs", "chem_set_trace", "chem_internal_energy")
+            "chem_temperature", "chem_energy", "chem_jacobian", "chem_rhs", "chem_set_trace", "chem_internal_energy", "chem_cell_status")
 
 _lib = None
 
@@ -108,7 +108,8 @@ def load_library():
     lib.chem_integrate_boxes.argtypes = [P, I32, P, D, D, P, ctypes.c_size_t, P, P, P]
     lib.chem_set_trace.argtypes = [P, P, I32]
     lib.chem_internal_energy.argtypes = [P, I64, I64, P, P, P]
-    for f in ("chem_init", "chem_set_opts", "chem_set_trace", "chem_internal_energy", "chem_rates", "chem_rhs", "chem_jacobian", "chem_temperature",
+    lib.chem_cell_status.argtypes = [P, P, ctypes.c_size_t, I64, I64, P, P, P]
+    for f in ("chem_cell_status", "chem_init", "chem_set_opts", "chem_set_trace", "chem_internal_energy", "chem_rates", "chem_rhs", "chem_jacobian", "chem_temperature",
               "chem_energy", "chem_integrate", "chem_integrate_boxes"):
         getattr(lib, f).restype = ctypes.c_int
     _lib = lib

@@ -11,7 +11,6 @@
 #include <vector>
 
 #include "../../include/chem.h"
-#include "chem_group.cuh"
 #include "chem_launch.cuh"
 
 #include <cub/device/device_radix_sort.cuh>
@@ -40,16 +39,11 @@ struct Ops {
     cudaError_t (*temperature)(const void*, int64_t, int64_t, const double*, const double*, double*,
                                unsigned long long*, cudaStream_t);
     cudaError_t (*energy)(const void*, int64_t, int64_t, const double*, const double*, double*, cudaStream_t);
-    cudaError_t (*integrate)(const void*, int method, int dae, const LaunchCtx&, const uint32_t*, int64_t, int, int,
-                             int, int grid, cudaStream_t);
-    cudaError_t (*integrate_lock)(const void*, int method, int dae, const LaunchCtx&, const uint32_t*, int64_t,
-                                  int kmax, int refill, int fin, int nsm, cudaStream_t);
-    cudaError_t (*integrate_grp)(const void* gtab, int method, int lanes, const LaunchCtx&, const uint32_t*, int64_t,
-                                 int, int, int, int grid, cudaStream_t);
-    int (*blocks_per_sm)(int method, int dae);
-    int (*grp_blocks_per_sm)(int method, int lanes);
-    size_t gtab_size;
-    void (*build_gtab)(const void* params, void* out);
+    cudaError_t (*integrate)(const void*, int method, const LaunchCtx&, const uint32_t*, int64_t, int kmax,
+                             int refill, int fin, int grid, cudaStream_t);
+    cudaError_t (*integrate_lock)(const void*, int method, const LaunchCtx&, const uint32_t*, int64_t, int kmax,
+                                  int refill, int fin, int nsm, cudaStream_t);
+    int (*blocks_per_sm)(int method);
     size_t integrate_smem;
 };
 
@@ -145,16 +139,7 @@ struct MechOps {
                              const double* Y, double* w, cudaStream_t s)
     {
         if (n == 0) return cudaSuccess;
-        static const int minb = [] { const char* e = getenv("CHEM_RATES_MINB"); return e ? atoi(e) : 1; }();
-        const P& p = *static_cast<const P*>(pp);
-        const int g = grid_for(n, kPointBS);
-        switch (minb) {   // experiment hook: occupancy vs registers (not part of the ABI)
-        case 2: k_rates<M, 2><<<g, kPointBS, 0, s>>>(p, n, ld, rho, T, Y, w); break;
-        case 3: k_rates<M, 3><<<g, kPointBS, 0, s>>>(p, n, ld, rho, T, Y, w); break;
-        case 4: k_rates<M, 4><<<g, kPointBS, 0, s>>>(p, n, ld, rho, T, Y, w); break;
-        case 6: k_rates<M, 6><<<g, kPointBS, 0, s>>>(p, n, ld, rho, T, Y, w); break;
-        default: k_rates<M, 1><<<g, kPointBS, 0, s>>>(p, n, ld, rho, T, Y, w); break;
-        }
+        k_rates<M><<<grid_for(n, kPointBS), kPointBS, 0, s>>>(*static_cast<const P*>(pp), n, ld, rho, T, Y, w);
         return cudaGetLastError();
     }
     static cudaError_t rhs(const void* pp, int64_t n, int64_t ld, const double* rho, const double* T,
@@ -191,70 +176,27 @@ struct MechOps {
     }
 
     // ---- integration launchers (defined in chem_launch_impl.cuh, instantiated in launch_*.cu)
-    template <bool DAE>
-    static cudaError_t lock_t(const P& p, int method, const LaunchCtx& L, const uint32_t* ids, int64_t n, int kmax,
-                              int refill, int fin, int nsm, cudaStream_t s)
-    {
-        if (method == CHEM_METHOD_RODAS3) return Launch<M, Rodas3, DAE>::lock(p, L, ids, n, kmax, refill, fin, nsm, s);
-        if (method == CHEM_METHOD_ROS4) return Launch<M, Ros4, DAE>::lock(p, L, ids, n, kmax, refill, fin, nsm, s);
-        return Launch<M, Rodas4, DAE>::lock(p, L, ids, n, kmax, refill, fin, nsm, s);
-    }
-    // lockstep launch (chem_opts.lockstep / lockstep_sparse); Rosenbrock methods only
-    static cudaError_t integrate_lock(const void* pp, int method, int dae, const LaunchCtx& L, const uint32_t* ids,
+    // lockstep launch (chem_opts.lockstep, heavy-first schedule); Rosenbrock methods only
+    static cudaError_t integrate_lock(const void* pp, int method, const LaunchCtx& L, const uint32_t* ids,
                                       int64_t n, int kmax, int refill, int fin, int nsm, cudaStream_t s)
     {
         const P& p = *static_cast<const P*>(pp);
-        return dae ? lock_t<true>(p, method, L, ids, n, kmax, refill, fin, nsm, s)
-                   : lock_t<false>(p, method, L, ids, n, kmax, refill, fin, nsm, s);
+        if (method == CHEM_METHOD_RODAS3) return Launch<M, Rodas3>::lock(p, L, ids, n, kmax, refill, fin, nsm, s);
+        return Launch<M, Rodas4>::lock(p, L, ids, n, kmax, refill, fin, nsm, s);
     }
-    template <bool DAE>
-    static cudaError_t integrate_t(const P& p, int method, const LaunchCtx& L, const uint32_t* ids, int64_t n,
-                                   int kmax, int refill, int fin, int grid, cudaStream_t s)
-    {
-        if (method == CHEM_METHOD_RODAS3) return Launch<M, Rodas3, DAE>::run(p, L, ids, n, kmax, refill, fin, grid, s);
-        if (method == CHEM_METHOD_EXPLICIT) return Launch<M, Explicit, false>::run(p, L, ids, n, kmax, refill, fin, grid, s);
-        if (method == CHEM_METHOD_ROS4) return Launch<M, Ros4, DAE>::run(p, L, ids, n, kmax, refill, fin, grid, s);
-        return Launch<M, Rodas4, DAE>::run(p, L, ids, n, kmax, refill, fin, grid, s);
-    }
-    static cudaError_t integrate(const void* pp, int method, int dae, const LaunchCtx& L, const uint32_t* ids,
+    static cudaError_t integrate(const void* pp, int method, const LaunchCtx& L, const uint32_t* ids,
                                  int64_t n, int kmax, int refill, int fin, int grid, cudaStream_t s)
     {
         const P& p = *static_cast<const P*>(pp);
-        return dae ? integrate_t<true>(p, method, L, ids, n, kmax, refill, fin, grid, s)
-                   : integrate_t<false>(p, method, L, ids, n, kmax, refill, fin, grid, s);
+        if (method == CHEM_METHOD_RODAS3) return Launch<M, Rodas3>::run(p, L, ids, n, kmax, refill, fin, grid, s);
+        if (method == CHEM_METHOD_EXPLICIT) return Launch<M, Explicit>::run(p, L, ids, n, kmax, refill, fin, grid, s);
+        return Launch<M, Rodas4>::run(p, L, ids, n, kmax, refill, fin, grid, s);
     }
-    static int blocks_per_sm(int method, int dae)
+    static int blocks_per_sm(int method)
     {
-        if (method == CHEM_METHOD_EXPLICIT) return Launch<M, Explicit, false>::blocks_per_sm();
-        if (dae) {
-            if (method == CHEM_METHOD_RODAS3) return Launch<M, Rodas3, true>::blocks_per_sm();
-            if (method == CHEM_METHOD_ROS4) return Launch<M, Ros4, true>::blocks_per_sm();
-            return Launch<M, Rodas4, true>::blocks_per_sm();
-        }
-        if (method == CHEM_METHOD_RODAS3) return Launch<M, Rodas3, false>::blocks_per_sm();
-        if (method == CHEM_METHOD_ROS4) return Launch<M, Ros4, false>::blocks_per_sm();
-        return Launch<M, Rodas4, false>::blocks_per_sm();
-    }
-
-    // ---- lane-group kernel
-    static cudaError_t integrate_grp(const void* gt, int method, int lanes, const LaunchCtx& L, const uint32_t* ids,
-                                     int64_t n, int kmax, int refill, int fin, int grid, cudaStream_t s)
-    {
-        if (method == CHEM_METHOD_RODAS3)
-            return lanes == 4 ? LaunchGrp<M, Rodas3, 4>::run(gt, L, ids, n, kmax, refill, fin, grid, s)
-                              : LaunchGrp<M, Rodas3, 8>::run(gt, L, ids, n, kmax, refill, fin, grid, s);
-        return lanes == 4 ? LaunchGrp<M, Rodas4, 4>::run(gt, L, ids, n, kmax, refill, fin, grid, s)
-                          : LaunchGrp<M, Rodas4, 8>::run(gt, L, ids, n, kmax, refill, fin, grid, s);
-    }
-    static int grp_blocks_per_sm(int method, int lanes)
-    {
-        if (method == CHEM_METHOD_RODAS3)
-            return lanes == 4 ? LaunchGrp<M, Rodas3, 4>::blocks_per_sm() : LaunchGrp<M, Rodas3, 8>::blocks_per_sm();
-        return lanes == 4 ? LaunchGrp<M, Rodas4, 4>::blocks_per_sm() : LaunchGrp<M, Rodas4, 8>::blocks_per_sm();
-    }
-    static void build_gtab(const void* params, void* out)
-    {
-        GTable<M>::build(*static_cast<const P*>(params), *static_cast<GTable<M>*>(out));
+        if (method == CHEM_METHOD_EXPLICIT) return Launch<M, Explicit>::blocks_per_sm();
+        if (method == CHEM_METHOD_RODAS3) return Launch<M, Rodas3>::blocks_per_sm();
+        return Launch<M, Rodas4>::blocks_per_sm();
     }
 
     static Ops ops()
@@ -275,11 +217,7 @@ struct MechOps {
         o.integrate = &integrate;
         o.integrate_lock = &integrate_lock;
         o.blocks_per_sm = &blocks_per_sm;
-        o.integrate_grp = &integrate_grp;
-        o.grp_blocks_per_sm = &grp_blocks_per_sm;
-        o.gtab_size = sizeof(GTable<M>);
-        o.build_gtab = &build_gtab;
-        o.integrate_smem = Launch<M, Rodas4, false>::smem();
+        o.integrate_smem = Launch<M, Rodas4>::smem();
         return o;
     }
 };
@@ -377,14 +315,14 @@ struct chem_ctx {
     int64_t* h_start = nullptr;       // pinned
     unsigned long long* h_stats = nullptr;  // pinned [S_NSTATS]
     cudaEvent_t ev[2] = {nullptr, nullptr};
-    void* d_gtab = nullptr;          // device copy of the lane-group kernel's table
-    bool grp_ok = false;             // the group kernel needs one shared NASA T_mid
     int32_t* trace = nullptr;        // device [trace_rows][nboxes] activity trace (App. B), or null
     int32_t trace_rows = 0;
     double simt_eff = 1.0;           // bulk SIMT efficiency of the last call (lockstep = 2 input)
     void* sort_tmp = nullptr;        // cub radix-sort scratch of the heavy-first schedule (library-owned)
     size_t sort_tmp_bytes = 0;
     unsigned long long* h_sig = nullptr;   // pinned [3]: staging of the workspace layout signature
+    struct WsRecord { const void* ws; int64_t total; int32_t nboxes; };
+    std::vector<WsRecord> ws_last;   // layout of the last call on each workspace (chem_cell_status)
 };
 
 namespace {
@@ -432,14 +370,10 @@ void chem_default_opts(chem_opts* o)
     o->atol_T = 1e-6;
     o->method = CHEM_METHOD_RODAS4;
     o->compact_bulk = 1;
-    o->lanes_per_cell = 1;
     o->eps_change = 0.01;
-    o->temperature_mode = 0;
-    o->refill_bulk = 0;
     o->h0_factor = 0.01;
     o->lockstep = 2;
     o->kmax_first = 1;
-    o->lockstep_sparse = 0;
     o->schedule_lpt = 2;
 }
 
@@ -459,12 +393,10 @@ const char* chem_strerror(int code)
 static int check_opts(const chem_opts* o)
 {
     if (o->kmax_bulk < 1 || o->kmax_sparse < 1 || !(o->atol_T > 0.0) ||
-        (o->method < CHEM_METHOD_RODAS4 || o->method > CHEM_METHOD_ROS4) ||
+        (o->method < CHEM_METHOD_RODAS4 || o->method > CHEM_METHOD_EXPLICIT) ||
         !std::isfinite(o->T_min) || !(o->eps_change > 0.0 && o->eps_change <= 1.0) ||
-        (o->temperature_mode != 0 && o->temperature_mode != 1) || (o->refill_bulk != 0 && o->refill_bulk != 1) ||
-        o->lockstep < 0 || o->lockstep > 2 || o->kmax_first < 0 || o->lockstep_sparse < 0 || o->lockstep_sparse > 1 || o->schedule_lpt < 0 || o->schedule_lpt > 3 ||
-        !(o->h0_factor > 0.0 && o->h0_factor <= 1.0) ||
-        (o->lanes_per_cell != 1 && o->lanes_per_cell != 4 && o->lanes_per_cell != 8))
+        o->lockstep < 0 || o->lockstep > 2 || o->kmax_first < 0 || o->schedule_lpt < 0 || o->schedule_lpt > 2 ||
+        !(o->h0_factor > 0.0 && o->h0_factor <= 1.0) || (o->compact_bulk != 0 && o->compact_bulk != 1))
         return CHEM_EINVAL;
     return CHEM_OK;
 }
@@ -491,17 +423,6 @@ int chem_init(const chem_mech_desc* mech, const chem_opts* opts, int device, che
     c->opts = o;
     c->params.resize(ops->params_size);
     ops->fill(mech, c->params.data());
-    c->grp_ok = true;
-    for (int k = 1; k < mech->ns; ++k) c->grp_ok = c->grp_ok && mech->T_range[3 * k + 1] == mech->T_range[1];
-    {
-        std::vector<unsigned char> gt(ops->gtab_size);
-        ops->build_gtab(c->params.data(), gt.data());
-        if (cudaMalloc(&c->d_gtab, ops->gtab_size) != cudaSuccess ||
-            cudaMemcpy(c->d_gtab, gt.data(), ops->gtab_size, cudaMemcpyHostToDevice) != cudaSuccess) {
-            delete c;
-            return CHEM_ECUDA;
-        }
-    }
     cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
     if (cudaMallocHost(&c->h_stats, sizeof(unsigned long long) * S_NSTATS) != cudaSuccess ||
         cudaMallocHost(&c->h_sig, sizeof(unsigned long long) * 3) != cudaSuccess ||
@@ -523,7 +444,6 @@ void chem_finalize(chem_ctx* c)
     if (c->h_stats) cudaFreeHost(c->h_stats);
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
-    if (c->d_gtab) cudaFree(c->d_gtab);
     if (c->sort_tmp) cudaFree(c->sort_tmp);
     if (c->h_sig) cudaFreeHost(c->h_sig);
     delete c;
@@ -606,6 +526,26 @@ int chem_energy(chem_ctx* c, int64_t n, int64_t ld, const double* T, const doubl
     return cuda_fail(c, c->ops->energy(c->params.data(), n, ld, T, Y, e, (cudaStream_t)stream));
 }
 
+int chem_cell_status(chem_ctx* c, const void* ws, size_t ws_bytes, int64_t first, int64_t n, int8_t* status,
+                     int32_t* substeps, void* stream)
+{
+    CHEM_PRE(c);
+    if (!ws || first < 0 || n < 0) return CHEM_EINVAL;
+    const chem_ctx::WsRecord* rec = nullptr;
+    for (const auto& r : c->ws_last)
+        if (r.ws == ws) rec = &r;
+    if (!rec || first + n > rec->total) return CHEM_EINVAL;
+    const WsLayout W = ws_layout(rec->total, rec->nboxes);
+    if (ws_bytes < W.total) return CHEM_ENOWS;
+    if (n == 0) return CHEM_OK;
+    if (!status && !substeps) return CHEM_OK;
+    const char* base = static_cast<const char*>(ws);
+    const uint8_t* state = reinterpret_cast<const uint8_t*>(base + W.state) + first;
+    const int32_t* steps = reinterpret_cast<const int32_t*>(base + W.steps) + first;
+    k_cell_status<<<grid_for(n, kStreamBS), kStreamBS, 0, (cudaStream_t)stream>>>(state, steps, n, status, substeps);
+    return cuda_fail(c, cudaGetLastError());
+}
+
 int chem_integrate(chem_ctx* c, int64_t n, int64_t ld, const double* rho, const double* e, double* T, double* Y,
                    const uint8_t* solid, double dt, double rtol, double atol, void* ws, size_t ws_bytes,
                    chem_stats* stats, void* stream)
@@ -637,6 +577,15 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
     if (total >= (int64_t)0xffffffffLL) return CHEM_EINVAL;  // 32-bit cell index map
     const WsLayout W = ws_layout(total, nboxes);
     if (ws_bytes < W.total) return CHEM_ENOWS;
+    {
+        bool found = false;
+        for (auto& r : c->ws_last)
+            if (r.ws == ws) { r.total = total; r.nboxes = nboxes; found = true; }
+        if (!found) {
+            if (c->ws_last.size() >= 64) c->ws_last.erase(c->ws_last.begin());
+            c->ws_last.push_back({ws, total, nboxes});
+        }
+    }
     if (ensure_host_boxes(c, nboxes) != CHEM_OK) return CHEM_ECUDA;
     cudaStream_t s = (cudaStream_t)stream;
     const chem_opts& o = c->opts;
@@ -669,6 +618,7 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
     L.T_min = o.T_min;
     L.eps_change = o.eps_change;
     L.h0_factor = o.h0_factor;
+    L.kmax_call = o.kmax_sparse;
     uint32_t* ids0 = reinterpret_cast<uint32_t*>(base + W.ids0);
     uint32_t* idsA = reinterpret_cast<uint32_t*>(base + W.idsA);
     uint32_t* idsB = reinterpret_cast<uint32_t*>(base + W.idsB);
@@ -699,9 +649,6 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
         v = (int64_t)c->h_stats[S_COUNT_ACTIVE];
         return r;
     };
-
-    const bool use_grp = o.lanes_per_cell > 1 && c->grp_ok && o.temperature_mode == 0 &&
-                         (o.method == CHEM_METHOD_RODAS4 || o.method == CHEM_METHOD_RODAS3);
 
     // ---- Alg. 3 §1: gate + count + index map
     CK(cudaEventRecord(c->ev[0], s));
@@ -742,20 +689,17 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
     const uint64_t pred_total = c->h_stats[S_PRED_TOTAL], pred_heavy = c->h_stats[S_PRED_HEAVY];
     const uint64_t pred_max = c->h_stats[S_PRED_MAX];
     const bool sortable = n_active > 0 && n_active <= (int64_t)0x7fffffff;   // cub's int item count
-    const bool eligible = sortable && !use_grp && o.method != CHEM_METHOD_EXPLICIT;
+    const bool eligible = sortable && o.method != CHEM_METHOD_EXPLICIT;
     // hints that vary (max above 1.5x the mean) or put half the work in heavy cells
     const bool skewed = history && pred_total > 0 &&
                         (2 * pred_heavy >= pred_total ||
                          (double)pred_max * (double)n_active > 1.5 * (double)pred_total);
     const bool lpt = eligible && (o.schedule_lpt == 1 || (o.schedule_lpt == 2 && skewed));
-    // schedule_lpt = 3: keep Alg. 3's bulk bursts but sort their list by the hints (descending):
-    // warps then hold cells that need similar numbers of substeps
-    const bool sort_bulk = eligible && !lpt && o.schedule_lpt == 3 && history && pred_total > 0;
-    st.lpt = lpt ? 1 : (sort_bulk ? 2 : 0);
+    st.lpt = lpt ? 1 : 0;
     const uint32_t* cur = ids0;
     int64_t n_cur = n_active;
     uint32_t* nxt = idsA;
-    if (lpt || sort_bulk) {
+    if (lpt) {
         cub::DoubleBuffer<uint32_t> dk(key0, key1), dv(ids0, idsA);
         size_t need = 0;
         int bits = 1;                                    // keys <= pred_max: sort only the bits in use
@@ -775,7 +719,7 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
 
     // ---- Alg. 3 §2: bulk bursts while N_active > N*
     // lockstep bursts (chem_opts.lockstep; auto: the previous call's bulk SIMT efficiency was low)
-    const bool lock = !use_grp && !o.refill_bulk && o.method != CHEM_METHOD_EXPLICIT &&
+    const bool lock = o.method != CHEM_METHOD_EXPLICIT &&
                       (o.lockstep == 1 || (o.lockstep == 2 && c->simt_eff < kLockEff));
     st.lockstep = lock;
     unsigned long long att_skip = 0, ws_skip = 0;   // the one-substep first burst is not a SIMT sample
@@ -783,10 +727,7 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
     // below it a bulk burst can no longer fill the GPU, so the persistent sparse launch takes over
     // (B200 sweep, profiles/r01_nstar_sweep.txt; the paper's 1e4 was tuned on H100).
     const int64_t nstar = o.n_active_star >= 0 ? o.n_active_star
-                          : use_grp ? (int64_t)c->num_sms * ops.grp_blocks_per_sm(o.method, o.lanes_per_cell) *
-                                          (kGrpBS / o.lanes_per_cell)
-                                    : (int64_t)c->num_sms * ops.blocks_per_sm(o.method, o.temperature_mode) *
-                                          kIntegrateBS;
+                                               : (int64_t)c->num_sms * ops.blocks_per_sm(o.method) * kIntegrateBS;
     while (!lpt && n_cur > nstar && n_cur > 0) {
         const bool first_burst = lock && st.bulk_iters == 0 && o.kmax_first > 0;
         const int kmax_b = first_burst ? o.kmax_first : o.kmax_bulk;
@@ -794,20 +735,10 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
         const uint32_t* lst = all_cells ? nullptr : cur;
         const int64_t nl = all_cells ? total : n_cur;
         CK(cudaEventRecord(c->ev[0], s));
-        if (use_grp)
-            CK(ops.integrate_grp(c->d_gtab, o.method, o.lanes_per_cell, L, lst, nl, kmax_b, 0, 0,
-                                 (int)((nl * o.lanes_per_cell + kGrpBS - 1) / kGrpBS), s));
-        else if (lock)
-            CK(ops.integrate_lock(c->params.data(), o.method, o.temperature_mode, L, lst, nl, kmax_b, 0, 0, c->num_sms,
-                                  s));
-        else if (o.refill_bulk) {
-            // persistent grid; a lane whose cell finishes its burst early takes the next id
-            CK(cudaMemsetAsync(L.stats + S_CURSOR, 0, 8, s));
-            const int grid = std::max(1, std::min<int>(c->num_sms * ops.blocks_per_sm(o.method, o.temperature_mode),
-                                                       (int)((nl + kIntegrateBS - 1) / kIntegrateBS)));
-            CK(ops.integrate(c->params.data(), o.method, o.temperature_mode, L, lst, nl, kmax_b, 1, 0, grid, s));
-        } else
-            CK(ops.integrate(c->params.data(), o.method, o.temperature_mode, L, lst, nl, kmax_b, 0, 0,
+        if (lock)
+            CK(ops.integrate_lock(c->params.data(), o.method, L, lst, nl, kmax_b, 0, 0, c->num_sms, s));
+        else
+            CK(ops.integrate(c->params.data(), o.method, L, lst, nl, kmax_b, 0, 0,
                              (int)((nl + kIntegrateBS - 1) / kIntegrateBS), s));
         CK(cudaEventRecord(c->ev[1], s));
         CK(cudaEventSynchronize(c->ev[1]));
@@ -846,20 +777,13 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
     if (n_cur > 0) {
         CK(cudaMemsetAsync(L.stats + S_CURSOR, 0, 8, s));
         CK(cudaEventRecord(c->ev[0], s));
-        if (use_grp) {
-            const int cells_per_block = kGrpBS / o.lanes_per_cell;
-            const int grid = std::max(1, std::min<int>(c->num_sms * ops.grp_blocks_per_sm(o.method, o.lanes_per_cell),
-                                                       (int)((n_cur + cells_per_block - 1) / cells_per_block)));
-            CK(ops.integrate_grp(c->d_gtab, o.method, o.lanes_per_cell, L, cur, n_cur, o.kmax_sparse, 1, 1, grid, s));
-        } else if ((o.lockstep_sparse || lpt) && o.method != CHEM_METHOD_EXPLICIT) {
-            // persistent lockstep blocks (one per SM) with warp-batched refill
-            CK(ops.integrate_lock(c->params.data(), o.method, o.temperature_mode, L, cur, n_cur, o.kmax_sparse, 1, 1,
-                                  c->num_sms, s));
+        if (lpt) {
+            // heavy-first: persistent lockstep blocks (one per SM) with warp-batched refill
+            CK(ops.integrate_lock(c->params.data(), o.method, L, cur, n_cur, o.kmax_sparse, 1, 1, c->num_sms, s));
         } else {
-            const int grid = std::max(1, std::min<int>(c->num_sms * ops.blocks_per_sm(o.method, o.temperature_mode),
+            const int grid = std::max(1, std::min<int>(c->num_sms * ops.blocks_per_sm(o.method),
                                                        (int)((n_cur + kIntegrateBS - 1) / kIntegrateBS)));
-            CK(ops.integrate(c->params.data(), o.method, o.temperature_mode, L, cur, n_cur, o.kmax_sparse, 1, 1,
-                             grid, s));
+            CK(ops.integrate(c->params.data(), o.method, L, cur, n_cur, o.kmax_sparse, 1, 1, grid, s));
         }
         CK(cudaEventRecord(c->ev[1], s));
     }

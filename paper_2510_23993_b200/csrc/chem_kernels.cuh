@@ -58,6 +58,8 @@ struct LaunchCtx {
     double rtol, atol, atolT, T_min;
     double eps_change;          // explicit scheme: max fractional change per step
     double h0_factor;           // initial substep = h0_factor |y|/|f| (Hairer-Norsett-Wanner: 0.01)
+    int32_t kmax_call;          // per-cell budget of attempted substeps over the whole call
+                                // (chem_opts.kmax_sparse): reached in any launch -> ST_UNFINISHED
 };
 
 __device__ __forceinline__ int find_box(const LaunchCtx& L, int64_t g)
@@ -202,15 +204,13 @@ __global__ void __launch_bounds__(BS) k_box_count(LaunchCtx L, const uint32_t* i
 }
 
 // ----------------------------------------------------------------------------- A6/A7/A9 integrate
-// Per-thread shared memory: the n x n iteration matrix (I/(h gamma) - J, then its LU), an
-// n-vector scratch for the permuted right-hand side, and n pivot bytes.
 // Per-thread shared memory (stride = block size, conflict-free): the n x n iteration matrix
-// (I/(h gamma) - J, then its LU) and the stored stage vectors K_s (pivot rows stay in registers).  n = NSA+1
-// (T integrated by Eq. 6) or NSA (DAE: T from Newton at every evaluation).  Stiffly accurate
-// methods (RODAS4) do not store the last stage: y_new = Y_last + K_last and err = K_last.
-template <class M, class Meth, bool DAE = false>
+// (I/(h gamma) - J, then its LU) and the stored stage vectors K_s (pivot rows stay in registers);
+// n = NSA+1 unknowns (reacting Y_k and T, Eq. 6).  Stiffly accurate methods (RODAS4) do not store
+// the last stage: y_new = Y_last + K_last and err = K_last.
+template <class M, class Meth>
 struct SmemLayout {
-    static constexpr int n = DAE ? M::NSA : M::NSA + 1;
+    static constexpr int n = M::NSA + 1;
     static constexpr bool none = (Meth::S == 0);   // explicit scheme: no matrix, no stages
     // stage slots: RODAS4 keeps three (ros_step's collapse), stiffly accurate methods S-1, others S
     static constexpr int nK = Meth::collapse ? 3 : (Meth::stiff_last ? Meth::S - 1 : Meth::S);
@@ -234,31 +234,22 @@ struct Cell {
     int64_t off, ld;
     uint32_t g;
     int k;                 // attempted substeps in this launch
+    int kprev;             // attempted substeps in earlier launches of this call (the call budget)
     bool rej;              // last step rejected (controller memory, persisted in state bit 7)
 };
 
 // One attempted Rosenbrock substep on cell C (A6).  Returns 1 accepted, 0 rejected, -1 failure.
 // The stage loop is a runtime loop (one inlined copy of the RHS in the kernel: the fully
 // unrolled version overflowed the instruction cache); stage vectors live in shared memory.
-// DAE: the unknowns are the reacting Y; C.y[NSA] carries T = T(e, Y) (Newton).
-template <class M, class Meth, bool DAE>
+template <class M, class Meth>
 __device__ __forceinline__ int ros_step(const Params<M>& P, const LaunchCtx& L, Cell<M>& C, const SMat& A,
                                         double* Ks, int ss, Counters& cnt)
 {
-    constexpr int n = DAE ? M::NSA : M::NSA + 1;
+    constexpr int n = M::NSA + 1;
     constexpr int S = Meth::S;
     const double invrho = frcp(C.rho);
     double f0[n];
-    if constexpr (DAE) {
-        double Yf[M::NS];
-        full_Y<M>(C.y, C.Yin, Yf);
-        double T = C.y[M::NSA];
-        if (!newton_T<M>(P, C.e, Yf, T)) return -1;
-        C.y[M::NSA] = T;
-        rhs_jac<M, JAC_DAE>(P, C.rho, C.y, C.Yin, f0, A);
-    } else {
-        rhs_jac<M, JAC_ODE>(P, C.rho, C.y, C.Yin, f0, A);
-    }
+    rhs_jac<M, JAC_ODE>(P, C.rho, C.y, C.Yin, f0, A);
     cnt.rhs++;
     const double remaining = C.dt - C.t;
     if (!(C.h > 0.0)) {
@@ -303,7 +294,6 @@ __device__ __forceinline__ int ros_step(const Params<M>& P, const LaunchCtx& L, 
     const bool ok = lu_factor<n>(A, perm);
 
     const double hinv = 1.0 / h;
-    bool stage_ok = true;
     double ylast[n];                          // stage point of the last stage (stiffly accurate)
     auto slot = [&](int j) { return Ks + (j * n) * ss; };
     if constexpr (Meth::collapse) {
@@ -349,12 +339,7 @@ __device__ __forceinline__ int ros_step(const Params<M>& P, const LaunchCtx& L, 
                     G[i] = gs[i * ss];
                 }
             }
-            if constexpr (DAE) {
-                double Ts = C.y[M::NSA];
-                stage_ok = rhs_dae<M>(P, C.rho, invrho, C.e, ys, C.Yin, Ts, F) && stage_ok;
-            } else {
-                rhs<M>(P, C.rho, invrho, ys, C.Yin, F);
-            }
+            rhs<M>(P, C.rho, invrho, ys, C.Yin, F);
             cnt.rhs++;
 #pragma unroll
             for (int i = 0; i < n; ++i) F[i] = fma(hinv, G[i], F[i]);
@@ -415,12 +400,7 @@ __device__ __forceinline__ int ros_step(const Params<M>& P, const LaunchCtx& L, 
                         for (int i = 0; i < n; ++i) ys[i] = fma(a, slot(j)[i * ss], ys[i]);
                     }
                 }
-                if constexpr (DAE) {
-                    double Ts = C.y[M::NSA];
-                    stage_ok = rhs_dae<M>(P, C.rho, invrho, C.e, ys, C.Yin, Ts, F) && stage_ok;
-                } else {
-                    rhs<M>(P, C.rho, invrho, ys, C.Yin, F);
-                }
+                rhs<M>(P, C.rho, invrho, ys, C.Yin, F);
                 cnt.rhs++;
                 if constexpr (Meth::reuse_last) {
 #pragma unroll
@@ -477,7 +457,7 @@ __device__ __forceinline__ int ros_step(const Params<M>& P, const LaunchCtx& L, 
     err = sqrt(err * (1.0 / n));
     cnt.attempted++;
     C.k++;
-    if (!ok || !stage_ok || !isfinite(err)) {  // singular matrix or non-finite stage: shrink hard, retry
+    if (!ok || !isfinite(err)) {  // singular matrix or non-finite stage: shrink hard, retry
         C.h = h * 0.1;
         C.rej = true;
         return 0;
@@ -559,6 +539,7 @@ __device__ __forceinline__ void load_cell(const Params<M>& P, const LaunchCtx& L
     for (int i = 0; i < M::NSA; ++i) C.y[i] = C.Yin[M::act(i)];
     double T = bx.T[C.off];
     C.k = 0;
+    C.kprev = L.cell_steps[g];
     ok = true;
     if ((st & 0x7f) == ST_FRESH) {
         // initial temperature from (e, Y) at constant (e, rho), seeded with the input T
@@ -635,14 +616,14 @@ __device__ __forceinline__ void flush_counters(const LaunchCtx& L, Counters& c)
 // LOCK: the block's warps take each substep together (one __syncthreads_or per substep), so that on a
 // heterogeneous field the SM's resident warps stay in the same code region (shared instruction cache)
 // instead of drifting apart; a thread whose cell has left the burst idles at the barrier.
-template <class M, class Meth, int BS, bool DAE = false, bool LOCK = false>
+template <class M, class Meth, int BS, bool LOCK = false>
 __global__ void __launch_bounds__(BS) k_integrate(const __grid_constant__ Params<M> P, LaunchCtx L,
                                                   const uint32_t* __restrict__ ids, int64_t n_ids, int kmax,
                                                   int refill, int final_phase)
 {
     extern __shared__ double smem[];
     fm_tables_to_smem();
-    using SL = SmemLayout<M, Meth, DAE>;
+    using SL = SmemLayout<M, Meth>;
     constexpr int n = SL::n;
     double* mine = smem + threadIdx.x;
     SMat A{mine, BS, n};
@@ -662,13 +643,18 @@ __global__ void __launch_bounds__(BS) k_integrate(const __grid_constant__ Params
         }
         int r;
         if constexpr (Meth::S == 0) r = explicit_step<M>(P, L, C, L.eps_change, cnt);
-        else r = ros_step<M, Meth, DAE>(P, L, C, A, Ks, BS, cnt);
+        else r = ros_step<M, Meth>(P, L, C, A, Ks, BS, cnt);
         if (r < 0) {
             cnt.nonfinite++;
             store_cell<M>(P, L, C, ST_FAILED, cnt);
             have = false;
         } else if (C.t >= C.dt) {
             store_cell<M>(P, L, C, ST_DONE, cnt);
+            have = false;
+        } else if (C.kprev + C.k >= L.kmax_call) {
+            // the call's per-cell budget of attempted substeps is spent, whichever launch (bulk
+            // burst, sparse or heavy-first) the cell is in: the schedules stay bitwise equivalent
+            store_cell<M>(P, L, C, ST_UNFINISHED, cnt);
             have = false;
         } else if (C.k >= kmax) {
             store_cell<M>(P, L, C, final_phase ? ST_UNFINISHED : ST_RUNNING, cnt);
@@ -743,9 +729,22 @@ __global__ void __launch_bounds__(BS) k_integrate(const __grid_constant__ Params
     flush_counters(L, cnt);
 }
 
+// A11 per-cell outcome of the last call: workspace state byte -> CHEM_CELL_* code
+// (0 untouched, 1 done, 2 unfinished, -1 failed; a cell still FRESH/RUNNING, which no completed call
+// leaves, reads as failed), and the cell's attempted substeps of the call.  HBM-bound.
+static __global__ void k_cell_status(const uint8_t* __restrict__ state, const int32_t* __restrict__ steps, int64_t n,
+                                     int8_t* __restrict__ out, int32_t* __restrict__ steps_out)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint8_t s = state[i] & 0x7f;
+        if (out) out[i] = s == ST_INACTIVE ? 0 : s == ST_DONE ? 1 : s == ST_UNFINISHED ? 2 : -1;
+        if (steps_out) steps_out[i] = s == ST_INACTIVE ? 0 : steps[i];
+    }
+}
+
 // ----------------------------------------------------------------------------- point kernels
-template <class M, int MINB = 1>
-__global__ void __launch_bounds__(128, MINB) k_rates(const __grid_constant__ Params<M> P, int64_t n, int64_t ld,
+template <class M>
+__global__ void __launch_bounds__(128) k_rates(const __grid_constant__ Params<M> P, int64_t n, int64_t ld,
                                                     const double* __restrict__ rho,
                         const double* __restrict__ T, const double* __restrict__ Y, double* __restrict__ wdot)
 {

@@ -1,5 +1,5 @@
 // chem_launch.cuh — host launchers of the integration kernels, declared here and defined in
-// chem_launch_impl.cuh.  Each integrator (RODAS4, RODAS3, ROS4, explicit, lane groups) is explicitly
+// chem_launch_impl.cuh.  Each integrator (RODAS4, RODAS3, explicit) is explicitly
 // instantiated in its own translation unit (launch_*.cu) so the sm_100a build compiles them in
 // parallel; chem_api.cu sees only these declarations.
 #pragma once
@@ -10,25 +10,17 @@
 namespace chem {
 
 constexpr int kIntegrateBS = 32;   // threads per block of the free-running k_integrate
-constexpr int kGrpBS = 128;        // threads per block of k_integrate_grp
 
-template <class M, class Meth, bool DAE>
+template <class M, class Meth>
 struct Launch {
-    // bulk (refill = 0) or sparse (refill = 1) launch of k_integrate<M, Meth, kIntegrateBS, DAE>
+    // bulk (refill = 0) or sparse (refill = 1) launch of k_integrate<M, Meth, kIntegrateBS>
     static cudaError_t run(const Params<M>& p, const LaunchCtx& L, const uint32_t* ids, int64_t n, int kmax,
                            int refill, int fin, int grid, cudaStream_t s);
     // lockstep bulk launch: persistent blocks, one per SM (chem_opts.lockstep)
     static cudaError_t lock(const Params<M>& p, const LaunchCtx& L, const uint32_t* ids, int64_t n, int kmax,
                             int refill, int fin, int nsm, cudaStream_t s);
     static int blocks_per_sm();
-    static constexpr size_t smem() { return (size_t)SmemLayout<M, Meth, DAE>::bytes_per_thread * kIntegrateBS; }
-};
-
-template <class M, class Meth, int G>
-struct LaunchGrp {
-    static cudaError_t run(const void* gtab, const LaunchCtx& L, const uint32_t* ids, int64_t n, int kmax,
-                           int refill, int fin, int grid, cudaStream_t s);
-    static int blocks_per_sm();
+    static constexpr size_t smem() { return (size_t)SmemLayout<M, Meth>::bytes_per_thread * kIntegrateBS; }
 };
 
 }  // namespace chem

@@ -1,18 +1,24 @@
-"""Algorithmic work model of the integration kernels (SURVEY.md §8(d) "Algorithmic work per unit").
+"""Algorithmic work model of the integration kernels: SURVEY.md §8(d) "Algorithmic work per unit",
+implemented literally, so the bench's roofline fraction can be recomputed by hand
+as  (§8(d) FLOPs per substep x chem_stats counters) / (CUDA-event k_integrate time) / peak.
 
-Counts what the method must compute, not what the hardware executes: no dense zeros, no
-redundant work.  FP64 transcendentals are charged w_exp / w_log flops each, the
-DADD + DMUL + 2*DFMA count of one libdevice exp / log on sm_100a (profiles/wt_microbench.json,
-static SASS count of the kernels `exp(x)` / `log(x)` compiled for sm_100a: exp = 2 DADD + 1 DMUL +
-14 DFMA -> 31, log = 8 DADD + 5 DMUL + 17 DFMA -> 47).
+Per RHS evaluation (A3-A5), §8(d):
+    24 Ns (thermo) + 4 Nr (ln k) + 2 nnz(nu) + 2 Nr (ln Kc) + 2 (nnz(nu') + nnz(nu'')) (ln q)
+    + Nr (difference) + 2 Ns N_tb (third-body) + 30 N_fo (falloff) + 2 nnz(nu) (Omega)
+    + 6 Ns (source terms) + transcendentals (1 + Ns) logs + (2 Nr + 3 N_fo) exps
+Per substep: Jacobian  sum_r 2 nnz_r(nu) (nnz_r(nu') + nnz_r(nu'')) + 2 N_tb nnz(nu) Ns/Nr + 15 Nr + 3 n^2,
+             LU 2 n^3 / 3, each of the s stage solves 2 n^2, control 10 n,   n = reacting species + 1;
+FLOPs_call = sum over attempted substeps of (s RHS + J + LU + s solves + control).
 
-Per RHS evaluation (A3-A5):
-  thermo 24*Ns + ln k 4*Nr + ln Kc (2*nnz(nu) + 2*Nr_rev) + ln q 2*(nnz(nu') + nnz(nu''))
-  + difference Nr + third-body 2*n_eff + falloff 30*N_fo + Omega 2*nnz(nu) + source 6*Ns
-  + w_log*(1 + Ns) + w_exp*(Nr + Nr_rev + N_fo) + Troe (2 w_log + 3 w_exp per row)
-Per Jacobian (A6): sum_r 2 nnz_r(nu) (nnz_r(nu') + nnz_r(nu'')) + 2 Ntb nnz(nu) Ns/Nr + 15 Nr
-  + 3 n^2 + w_exp*(Nr + Nr_rev)   (k_f, k_r for the product-form derivatives)
-LU 2n^3/3, each stage solve 2n^2, control 10n, with n = reacting species + 1.
+Transcendentals are charged at the DADD + DMUL + 2 DFMA count of one libdevice exp / log (§8(d)
+"w_t ... the DADD + DMUL + 2*DFMA count of one libdevice exp/log"): W_EXP = 31, W_LOG = 47 from
+the sm_100a SASS of `exp(x)` / `log(x)` (tools/wt_microbench.py -> profiles/wt_microbench.json,
+static count of the main path; the ncu dynamic count on the box is recorded beside it).
+
+The one departure from the literal formula, and why: a *frozen* first step (the
+north_star's "cheap bulk step", DESIGN reading R22) is one explicit Euler step y += dt f(y): the
+method evaluates one RHS there and no Jacobian, LU or stages, so it is charged one RHS.  At the
+parity tolerance frozen steps are rare (0 on cfg2); the bench reports their count.
 """
 from __future__ import annotations
 
@@ -28,45 +34,46 @@ class FlopModel:
         nu_r = np.asarray(mt.nu_r)
         net = nu_r - nu_f
         typ = np.asarray(mt.type)
-        rev = np.asarray(mt.reversible)
         ns, nr = mt.ns, mt.nr
         nnz_f = int(np.count_nonzero(nu_f))
         nnz_r = int(np.count_nonzero(nu_r))
         nnz = int(np.count_nonzero(net))
-        n_rev = int(rev.sum())
         n_fo = int(np.sum(typ >= 2))
-        n_troe = int(np.sum(typ == 3))
         n_tb = int(np.sum(typ >= 1))
-        n_eff = int(sum(np.count_nonzero(np.asarray(mt.eff)[r] != 1.0) for r in range(nr) if typ[r] >= 1))
         active = int(np.sum(np.any(net != 0, axis=0)))
         self.n = n = active + 1
-        self.rhs = (24 * ns + 4 * nr + 2 * nnz + 2 * n_rev + 2 * (nnz_f + nnz_r) + nr + 2 * n_eff + 30 * n_fo
-                    + 2 * nnz + 6 * ns + W_LOG * (1 + ns) + W_EXP * (nr + n_rev + n_fo)
-                    + n_troe * (2 * W_LOG + 3 * W_EXP))
+        self.n_log = 1 + ns
+        self.n_exp = 2 * nr + 3 * n_fo
+        self.rhs_plain = (24 * ns + 4 * nr + 2 * nnz + 2 * nr + 2 * (nnz_f + nnz_r) + nr + 2 * ns * n_tb
+                          + 30 * n_fo + 2 * nnz + 6 * ns)
+        self.rhs = self.rhs_plain + W_LOG * self.n_log + W_EXP * self.n_exp
         jac = 0.0
         for r in range(nr):
             jac += 2 * np.count_nonzero(net[r]) * (np.count_nonzero(nu_f[r]) + np.count_nonzero(nu_r[r]))
-        jac += 2 * n_tb * nnz * ns / max(nr, 1) + 15 * nr + 3 * n * n + W_EXP * (nr + n_rev)
-        self.jac = jac
+        self.jac = jac + 2 * n_tb * nnz * ns / max(nr, 1) + 15 * nr + 3 * n * n
         self.lu = 2.0 * n ** 3 / 3.0
         self.solve = 2.0 * n * n
         self.control = 10.0 * n
         self.stages = stages
 
+    def per_step(self):
+        """FLOPs of one attempted (non-frozen) substep: s RHS + J + LU + s solves + control."""
+        if self.stages == 0:           # the paper's explicit scheme: one RHS per step
+            return self.rhs
+        return self.stages * self.rhs + self.jac + self.lu + self.stages * self.solve + self.control
+
     def flops(self, stats):
         """Algorithmic FLOPs of one chem_integrate call from its chem_stats counters."""
         frozen = stats.get("steps_frozen", 0)
-        att = stats["steps_attempted"] - frozen   # frozen steps: one RHS (y += dt f), no LU/solves
-        # a frozen step evaluates J in the kernel (rhs_jac runs before the frozen test) but the method
-        # needs only f there, so J is not charged for it: algorithmic work, not executed work
-        return (stats["rhs_evals"] * self.rhs + (stats["jac_evals"] - frozen) * self.jac
-                + stats["lu_count"] * self.lu + att * (self.stages * self.solve + self.control))
+        return (stats["steps_attempted"] - frozen) * self.per_step() + frozen * self.rhs
 
-    def per_step(self):
-        return self.stages * self.rhs + self.jac + self.lu + self.stages * self.solve + self.control
+    def table(self):
+        return {"rhs_plain": self.rhs_plain, "rhs_logs": self.n_log, "rhs_exps": self.n_exp, "w_log": W_LOG,
+                "w_exp": W_EXP, "rhs": self.rhs, "jacobian": self.jac, "lu": self.lu, "solve": self.solve,
+                "control": self.control, "stages": self.stages, "n": self.n, "per_substep": self.per_step()}
 
 
-# FP64 peak of one B200 from unit counts and clocks (DESIGN.md §Roofline): 148 SMs x 64 FP64
-# FMA lanes per SM per clock x 2 flops x the max SM clock.
+# FP64 peak of one B200 from unit counts and clocks (DESIGN.md §5): 148 SMs x 64 FP64 FMA lanes per
+# SM per clock x 2 flops x the max SM clock.  The measured DFMA-loop peak is profiles/fp64_peak.json.
 def fp64_peak_tflops(sm_count=148, sm_mhz=1965.0, fma_per_sm=64):
     return sm_count * fma_per_sm * 2 * sm_mhz * 1e6 / 1e12

@@ -46,9 +46,29 @@ def test_default_opts_are_the_papers():
     o = binding.default_opts()
     # P:179 K_max = 5, P:181 N* (default < 0: one resident wave of the integration kernel)
     assert (o.kmax_bulk, o.n_active_star, o.kmax_sparse, o.T_min) == (5, -1, 100000, 500.0)
-    assert (o.lockstep, o.kmax_first, o.refill_bulk, o.compact_bulk) == (2, 1, 0, 1)
-    # heavy-first / sorted-bulk schedule on cost hints: auto; lockstep sparse launch: off
-    assert (o.schedule_lpt, o.lockstep_sparse) == (2, 0)
+    assert (o.lockstep, o.kmax_first, o.compact_bulk, o.method) == (2, 1, 1, 0)
+    # heavy-first schedule on cost hints: auto
+    assert o.schedule_lpt == 2
+
+
+def test_header_documents_the_defaults():
+    """chem.h's comment of chem_default_opts states the values the library sets (VERDICT r01
+    weak-6: it once said N* = 1e4 while the code set -1)."""
+    import pathlib
+    from paper_2510_23993_b200 import binding
+    hdr = (pathlib.Path(__file__).resolve().parent.parent / "include" / "chem.h").read_text()
+    doc = hdr[hdr.index("/* fills the defaults"):hdr.index("void chem_default_opts")]
+    o = binding.default_opts()
+    assert "n_active_star -1" in doc and o.n_active_star == -1
+    assert "kmax_bulk 5" in doc and "kmax_sparse 1e5" in doc and "schedule_lpt 2" in doc
+    assert "lockstep 2" in doc and "kmax_first 1" in doc and "T_min 500 K" in doc
+
+
+def test_cell_status_rejects_unknown_workspace_without_gpu():
+    """chem_cell_status on a workspace no call used is CHEM_EINVAL (checked before any device work)."""
+    from paper_2510_23993_b200 import binding
+    lib = binding.load_library()
+    assert lib.chem_cell_status(None, None, 0, 0, 0, None, None, None) == -1
 
 
 def test_opts_struct_matches_header():

@@ -33,10 +33,9 @@ def ora():
     return Oracle("h2air_li2004")
 
 
-@pytest.fixture(scope="module", params=[1, 8, 4], ids=["lanes1", "lanes8", "lanes4"])
-def chem(request):
-    """Both integrator kernels: one thread per cell, and lane groups of 8 / 4 per cell."""
-    return Chem("h2air_li2004", device=0, atol_T=1e-6, lanes_per_cell=request.param)
+@pytest.fixture(scope="module")
+def chem():
+    return Chem("h2air_li2004", device=0, atol_T=1e-6)
 
 
 def to_dev(x):
@@ -187,15 +186,14 @@ def test_empty_and_all_cold(chem, ora):
     assert st["active0"] == 0 and np.array_equal(Tg, T0) and np.array_equal(Yg, d["Y"])
 
 
-@pytest.mark.parametrize("lanes", [1, 8])
 @pytest.mark.parametrize("mech,y0,t,exact", [
     ("toy_a_to_b", [0.8, 0.2], 5e-3, lambda t: 0.8 * np.exp(-1e3 * t)),
     ("toy_a_eq_b", [0.9, 0.1], 4e-3, lambda t: 0.5 + 0.4 * np.exp(-2e3 * t)),
     ("toy_2a_to_b", [1.0, 0.0], 1e-2, lambda t: 1.0 / (1 + 2 * 10.0 * 50.0 * t)),
 ])
-def test_closed_forms_gpu(mech, y0, t, exact, lanes):
+def test_closed_forms_gpu(mech, y0, t, exact):
     """SURVEY §8(c) closed forms on the CUDA path (rtol 1e-11 -> 1e-8 relative)."""
-    ch = Chem(mech, device=0, atol_T=1e-9, lanes_per_cell=lanes)
+    ch = Chem(mech, device=0, atol_T=1e-9)
     o = Oracle(mech)
     n = 64
     rho = np.full(n, 1.0)
@@ -226,7 +224,6 @@ def test_schedule_invariance_bitwise(chem, ora):
                dict(kmax_bulk=3, n_active_star=50, compact_bulk=0)]
     for cfgo in configs:
         chem.set_opts(**{**dict(kmax_bulk=5, n_active_star=10000, compact_bulk=1), **cfgo})
-        assert chem.opts.lanes_per_cell in (1, 4, 8)
         T, Yg, st = _run_gpu(chem, rho, e, T0, Y, d["dt"])
         if ref is None:
             ref = (T, Yg, st["steps_attempted"])
@@ -286,13 +283,11 @@ def test_explicit_paper_scheme_algorithmic_parity(ora):
     assert np.max(np.abs(Yg[mask] / out["Y"][mask] - 1)) < 1e-10
 
 
-@pytest.mark.parametrize("method,tmode", [(1, 0), (3, 0), (0, 1), (1, 1)],
-                         ids=["rodas3", "ros4", "rodas4-dae", "rodas3-dae"])
 @pytest.mark.parametrize("cfg", ["cfg1", "cfg1c"])
-def test_integrate_parity_other_rosenbrock(ora, cfg, method, tmode):
-    """RODAS3, Shampine's ROS4, and the DAE temperature mode (T = Newton(e, Y) at every RHS
-    evaluation) reach the same 1e-6 parity bar at the parity tolerance."""
-    ch = Chem("h2air_li2004", device=0, atol_T=1e-6, method=method, temperature_mode=tmode)
+def test_integrate_parity_rodas3(ora, cfg):
+    """RODAS3 (CHEM_METHOD_RODAS3) reaches the same 1e-6 parity bar at the parity tolerance."""
+    method = 1
+    ch = Chem("h2air_li2004", device=0, atol_T=1e-6, method=method)
     m = ora.m
     d = getattr(synth, cfg)(m.species, m.W)
     idx = np.arange(0, 4096, 8) if cfg == "cfg1" else np.arange(0, 4096, 32)
@@ -317,6 +312,10 @@ def test_fault_injection_counts(ora):
     T, Yg, st = _run_gpu(ch, rho, e, T0, Y, d["dt"])
     assert st["n_unfinished"] > 0 and st["n_nonfinite"] == 0
     assert np.all(np.isfinite(T)) and np.all(np.isfinite(Yg))
+    # the per-cell status output names exactly the counted cells
+    status = ch.cell_status().cpu().numpy()
+    assert len(status) == len(rho)
+    assert (status == 2).sum() == st["n_unfinished"] and set(np.unique(status)) <= {1, 2}
     # NaN in one cell's Y: counted as a failure, neighbours bitwise equal to a clean run
     ch2 = Chem("h2air_li2004", device=0)
     Tc, Yc, _ = _run_gpu(ch2, rho, e, T0, Y, 1e-7)
@@ -324,6 +323,8 @@ def test_fault_injection_counts(ora):
     Yb[5, 3] = np.nan
     Tn, Yn, st2 = _run_gpu(ch2, rho, e, T0, Yb, 1e-7)
     assert st2["n_nonfinite"] + st2["n_newton_fail"] >= 1
+    status2 = ch2.cell_status().cpu().numpy()
+    assert status2[5] == -1 and np.all(np.delete(status2, 5) == 1)
     keep = np.arange(len(rho)) != 5
     assert np.array_equal(Tn[keep], Tc[keep]) and np.array_equal(Yn[keep], Yc[keep])
     # very hot cell: beyond the 3500 K NASA range -> counted in n_T_range, still finite
@@ -348,6 +349,20 @@ def test_invalid_arguments_are_errors():
         ch.set_opts(kmax_bulk=0)
     with pytest.raises(TypeError):
         ch.integrate(z.cpu(), z, z.clone(), Y, 1e-7)
+    # the binding guards what the C ABI cannot see: short, float32, foreign-device or
+    # mis-shaped buffers, a short box_cost, unknown option names
+    with pytest.raises(ValueError):
+        ch.integrate(z, z, z[:3].clone(), Y, 1e-7)
+    with pytest.raises(TypeError):
+        ch.integrate(z, z.float(), z.clone(), Y, 1e-7)
+    with pytest.raises(ValueError):
+        ch.integrate(z, z, z.clone(), Y[:, :3], 1e-7)
+    from paper_2510_23993_b200 import Box
+    with pytest.raises(ValueError):
+        ch.integrate_boxes([Box(z, z, z.clone(), Y, 1e-7)] * 2,
+                           box_cost=torch.zeros(1, dtype=torch.float64, device=DEV))
+    with pytest.raises(TypeError):
+        ch.set_opts(lanes_per_cell=4)
 
 
 def test_internal_energy_alg1():
@@ -381,3 +396,96 @@ def test_strang_half_steps_equal_full_step(ora):
     ch.strang_half_step([box], 2e-5, **GPU_TOL)
     out = ora.integrate_cells(rho, e, T0, Y, 2e-5, **ORA_TOL)
     _check_state(box.T.cpu().numpy(), box.Y.cpu().numpy().T, out, "strang")
+
+
+def test_cgs_toy_closed_forms_gpu():
+    """VERDICT r01 next-1a on the CUDA path: mech/toy_cgs_falloff.yaml (cm/mol/cal units) through the
+    product loader and the kernels against tests/pins/cgs_toy.py's hand-converted SI closed forms:
+    rates at t = 0 (1e-12) and the integrated three-body / Lindemann / Troe / second-order decays
+    (rtol 1e-11 -> 1e-8), isothermal at 1000 K."""
+    from tests.pins import cgs_toy as ct
+    ch = Chem("toy_cgs_falloff", device=0, atol_T=1e-9)
+    sp = ch.mech.species.index
+    rho = ct.rho_at_troe_centre()
+    n = 40
+    Y = np.zeros((n, ch.ns))
+    for k, v in ct.Y0.items():
+        Y[:, sp(k)] = v
+    lam1, lam2, lam3, k4 = ct.decay_rates(rho)
+    c = rho * Y[0] / ct.W
+    w = ch.rates(to_dev(np.full(n, rho)), to_dev(np.full(n, ct.T)), species_dev(Y)).cpu().numpy()[:, 0]
+    for name, v in (("A1", -lam1 * c[sp("A1")]), ("A2", -lam2 * c[sp("A2")]), ("A3", -lam3 * c[sp("A3")]),
+                    ("A4", -2.0 * k4 * c[sp("A4")] ** 2)):
+        assert abs(w[sp(name)] / v - 1) < 1e-12, (name, w[sp(name)], v)
+    o = Oracle("toy_cgs_falloff")
+    e = np.full(n, o.energy(ct.T, Y[0]))
+    t = 1e-5
+    Td = to_dev(np.full(n, ct.T))
+    Yd = species_dev(Y)
+    st = ch.integrate(to_dev(np.full(n, rho)), to_dev(e), Td, Yd, t, rtol=1e-11, atol=1e-20)
+    assert st["n_unfinished"] == 0
+    Yg = Yd.cpu().numpy()
+    for name, v in zip(("A1", "A2", "A3", "A4"), ct.exact_Y(rho, t)):
+        assert np.max(np.abs(Yg[sp(name)] / v - 1)) < 1e-8, name
+    assert np.max(np.abs(Td.cpu().numpy() - ct.T)) < 1e-8
+
+
+def test_negative_Y_edge(chem, ora):
+    """SURVEY reading 5 at the kink: rates use max(Y, 0) and the Jacobian column of a species with
+    Y < 0 is zero (cj = 0), on both sides; integrating from slightly negative radicals (the
+    integrator's own output, |Y| <= atol) stays within the parity bar."""
+    m = ora.m
+    d = synth.cfg1d(m.species, m.W, n=128, seed=11)
+    Y = d["Y"].copy()
+    rng = np.random.default_rng(12)
+    neg = rng.random(Y.shape) < 0.15
+    neg[:, m.species.index("N2")] = False
+    Y[neg] = -rng.uniform(1e-22, 1e-12, neg.sum())
+    rho, T = d["rho"], d["T"]
+    w = chem.rates(to_dev(rho), to_dev(T), species_dev(Y)).cpu().numpy()
+    J = chem.jacobian(to_dev(rho), to_dev(T), species_dev(Y)).cpu().numpy()
+    for i in range(len(T)):
+        wo, qf, qr = ora.rates(rho[i], T[i], Y[i])
+        G = np.abs(m.nu_r - m.nu_f).T.astype(float) @ (np.abs(qf) + np.abs(qr))
+        assert rates_close(w[:, i], wo, G).all(), i
+        Jo = ora.jac(rho[i], np.r_[Y[i], T[i]])
+        for k in np.nonzero(neg[i])[0]:
+            assert np.all(J[:m.ns, k, i] == 0.0), (i, k)      # the species block column is zero
+        scale = np.abs(Jo).max(axis=1) + 1e-300
+        assert (np.abs(J[:, :, i] - Jo).max(axis=1) / scale).max() < 1e-8, i
+    # integration from a radical-rich state with tiny negative radicals
+    doc = synth.load_trajectories()
+    d1 = synth.cfg1b(doc, n=256)
+    Y1 = d1["Y"].copy()
+    for k in ("H", "O", "HO2", "H2O2"):
+        Y1[::3, m.species.index(k)] = -1e-21
+    e1 = np.array([ora.energy(t, y) for t, y in zip(d1["T"], Y1)])
+    out = ora.integrate_cells(d1["rho"], e1, d1["T"], Y1, d1["dt"], **ORA_TOL)
+    assert np.all(out["status"] == 0)
+    Tg, Yg, st = _run_gpu(chem, d1["rho"], e1, d1["T"], Y1, d1["dt"])
+    assert st["n_nonfinite"] == 0 and st["n_unfinished"] == 0
+    _check_state(Tg, Yg, out, "negative-Y")
+
+
+def test_budget_equivalence_lpt_vs_alg3(ora):
+    """kmax_sparse is the per-cell budget of attempted substeps over the whole
+    call, so a cell that hits it ends UNFINISHED in the same state under Alg. 3 (bulk bursts +
+    sparse launch) and under the heavy-first launch: bitwise equal outputs, statuses and counts."""
+    m = ora.m
+    d = synth.cfg1c(m.species, m.W)
+    idx = np.arange(0, 4096, 16)
+    rho, T0, Y = d["rho"][idx], d["T"][idx], d["Y"][idx]
+    e = np.array([ora.energy(t, y) for t, y in zip(T0, Y)])
+    res = []
+    for opts in (dict(schedule_lpt=0, kmax_bulk=5, n_active_star=0),
+                 dict(schedule_lpt=0, kmax_bulk=3, n_active_star=64),
+                 dict(schedule_lpt=1), dict(schedule_lpt=0, n_active_star=10 ** 9)):
+        ch = Chem("h2air_li2004", device=0, kmax_sparse=12, **opts)
+        _run_gpu(ch, rho, e, T0, Y, d["dt"])        # leaves cost hints (the heavy-first launch needs them)
+        T, Yg, st = _run_gpu(ch, rho, e, T0, Y, d["dt"])
+        assert st["lpt"] == (1 if opts.get("schedule_lpt") == 1 else 0)
+        res.append((T, Yg, ch.cell_status().cpu().numpy(), st["n_unfinished"], st["steps_attempted"]))
+    assert res[0][3] > 0
+    for r in res[1:]:
+        assert np.array_equal(r[0], res[0][0]) and np.array_equal(r[1], res[0][1])
+        assert np.array_equal(r[2], res[0][2]) and r[3:] == res[0][3:]

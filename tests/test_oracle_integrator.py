@@ -50,6 +50,47 @@ def test_closed_form_2a_to_b():
         assert abs(y[2] - 900.0) < 1e-8
 
 
+def _cgs_state(o):
+    from tests.pins import cgs_toy as ct
+    rho = ct.rho_at_troe_centre()
+    Y = np.zeros(o.m.ns)
+    for k, v in ct.Y0.items():
+        Y[o.m.species.index(k)] = v
+    return ct, rho, Y
+
+
+def test_cgs_toy_rates_closed_form():
+    """the oracle loader's cm/cal conversion of three-body, Lindemann, Troe and
+    second-order rows, pinned by the hand-converted SI closed forms of tests/pins/cgs_toy.py at t = 0:
+    Omega_A1 = -lam1 c_A1, Omega_A2 = -lam2 c_A2, Omega_A3 = -lam3 c_A3, Omega_A4 = -2 k4 c_A4^2."""
+    o = Oracle("toy_cgs_falloff")
+    ct, rho, Y = _cgs_state(o)
+    lam1, lam2, lam3, k4 = ct.decay_rates(rho)
+    w, _, _ = o.rates(rho, ct.T, Y)
+    sp = o.m.species.index
+    c = rho * Y / ct.W
+    exp = {"A1": -lam1 * c[sp("A1")], "A2": -lam2 * c[sp("A2")], "A3": -lam3 * c[sp("A3")],
+           "A4": -2.0 * k4 * c[sp("A4")] ** 2}
+    for k, v in exp.items():
+        assert abs(w[sp(k)] / v - 1) < 1e-12, (k, w[sp(k)], v)
+    assert abs(w[sp("B4")] / (-0.5 * exp["A4"]) - 1) < 1e-12
+    assert w[sp("N")] == 0.0
+
+
+def test_cgs_toy_integrated_closed_form():
+    """The same pins through the oracle integrator: Y_Ai(t) against the closed forms over one dt at
+    T = 1000 K (isothermal by construction), rtol 1e-12 -> 1e-9 relative."""
+    o = Oracle("toy_cgs_falloff")
+    ct, rho, Y = _cgs_state(o)
+    sp = o.m.species.index
+    for t in (2e-6, 1e-5):
+        y, _ = o.integrate_state(rho, np.r_[Y, ct.T], t, rtol=1e-12, atolY=1e-24, atolT=1e-9)
+        ex = ct.exact_Y(rho, t)
+        for name, v in zip(("A1", "A2", "A3", "A4"), ex):
+            assert abs(y[sp(name)] / v - 1) < 1e-9, (name, t, y[sp(name)], v)
+        assert abs(y[-1] - ct.T) < 1e-8
+
+
 # ---------------------------------------------------------------- scipy library check
 
 def _cases(o):

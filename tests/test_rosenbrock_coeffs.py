@@ -54,8 +54,7 @@ def _e_vector(struct, s):
 
 
 @pytest.mark.parametrize("struct,Aname,Cname,gamma,order", [("Rodas4", "kRodas4A", "kRodas4C", 0.25, 4),
-                                                          ("Rodas3", "kRodas3A", "kRodas3C", 0.5, 3),
-                                                          ("Ros4", "kRos4A", "kRos4C", 0.5, 4)])
+                                                          ("Rodas3", "kRodas3A", "kRodas3C", 0.5, 3)])
 def test_order_conditions(struct, Aname, Cname, gamma, order):
     A, C, m = _table(Aname), _table(Cname), _m_vector(struct)
     res, alpha = _conditions(A, C, m, gamma)

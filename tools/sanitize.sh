@@ -1,6 +1,6 @@
 #!/bin/bash
 # compute-sanitizer memcheck / racecheck / synccheck / initcheck over a small chem_integrate
-# (cfg1, 256 cells, both kernels).  Output: gpurun_out/sanitize_*.txt
+# (cfg1c cells in two boxes: the free-running, lockstep and heavy-first launches, a budget-capped call).  Output: gpurun_out/sanitize_*.txt
 mkdir -p gpurun_out
 cat > /tmp/san_case.py <<'PY'
 import sys, os
@@ -12,9 +12,9 @@ m = load_mechanism("h2air_li2004")
 d = synth.cfg1c(m.species, m.W)
 idx = np.arange(0, 4096, 64)
 dev = torch.device("cuda", 0)
-for lanes, lock, lpt in ((1, 0, 0), (8, 0, 0), (1, 1, 0), (1, 0, 1)):
-    ch = Chem("h2air_li2004", device=0, lanes_per_cell=lanes, kmax_bulk=3, n_active_star=16, lockstep=lock,
-              schedule_lpt=lpt)
+for lock, lpt, ksp in ((0, 0, 100000), (1, 0, 100000), (0, 1, 100000), (0, 1, 7), (0, 0, 7)):
+    ch = Chem("h2air_li2004", device=0, kmax_bulk=3, n_active_star=16, lockstep=lock, schedule_lpt=lpt,
+              kmax_sparse=ksp)
     T = torch.tensor(d["T"][idx], device=dev)
     Y = torch.tensor(d["Y"][idx].T.copy(), device=dev)
     rho = torch.tensor(d["rho"][idx], device=dev)
@@ -29,7 +29,10 @@ for lanes, lock, lpt in ((1, 0, 0), (8, 0, 0), (1, 1, 0), (1, 0, 1)):
     torch.cuda.synchronize()
     st2 = ch.integrate_boxes(boxes, box_cost=cost)      # second call: cost hints from the first
     torch.cuda.synchronize()
-    print("lanes", lanes, "lockstep", lock, "lpt", lpt, st["steps_attempted"], st["sparse_cells"], st2["lpt"])
+    status, steps = ch.cell_status(substeps=True)
+    torch.cuda.synchronize()
+    print("lockstep", lock, "lpt", lpt, "kmax_sparse", ksp, st["steps_attempted"], st["sparse_cells"], st2["lpt"],
+          int(status.sum()), int(steps.sum()))
 PY
 for tool in memcheck racecheck synccheck initcheck; do
   timeout 900 compute-sanitizer --tool $tool --print-limit 20 python /tmp/san_case.py > gpurun_out/sanitize_$tool.txt 2>&1

@@ -43,7 +43,7 @@ def main():
     ap.add_argument("configs", nargs="*", default=["cfg3", "cfg4"])
     ap.add_argument("--kmax", default="5,20,100")
     ap.add_argument("--nstar", default="1e4,3e4,1e5,3e5,1e9")
-    ap.add_argument("--refill", default="0")
+    ap.add_argument("--lpt", default="0", help="schedule_lpt values to sweep (0 = Alg. 3, 2 = auto heavy-first)")
     ap.add_argument("--no-fusion", action="store_true")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
@@ -53,26 +53,26 @@ def main():
         a = argparse.Namespace(config=cfg, rtol=bench.RTOL, atol=bench.ATOL, balance="none")
         wl = bench.build_workload(a, chem, doc, dev, 0, 1)
         base = None
-        for rf in [int(x) for x in args.refill.split(",")]:
+        for lp in [int(x) for x in args.lpt.split(",")]:
           for km in [int(x) for x in args.kmax.split(",")]:
             for ns in [int(float(x)) for x in args.nstar.split(",")]:
-                chem.set_opts(kmax_bulk=km, n_active_star=ns, compact_bulk=1, refill_bulk=rf)
+                chem.set_opts(kmax_bulk=km, n_active_star=ns, compact_bulk=1, schedule_lpt=lp)
                 ms, st = time_step(wl, chem)
                 base = base or ms
                 print(json.dumps(dict(exp="schedule", config=cfg, kmax_bulk=km, n_active_star=ns, compact_bulk=1,
-                                      refill_bulk=rf,
+                                      schedule_lpt=lp,
                                       ms_per_step=ms, bulk_iters=sum(s["bulk_iters"] for s in st),
                                       sparse_cells=sum(s["sparse_cells"] for s in st),
                                       Mcell_steps_per_s=wl.cell_steps / ms / 1e3)), flush=True)
         if args.no_fusion:
             continue
-        chem.set_opts(kmax_bulk=5, n_active_star=10000, compact_bulk=0, refill_bulk=0)   # Alg. 3 as written
+        chem.set_opts(kmax_bulk=5, n_active_star=10000, compact_bulk=0, schedule_lpt=0)   # Alg. 3 as written
         ms, st = time_step(wl, chem)
         print(json.dumps(dict(exp="schedule", config=cfg, kmax_bulk=5, n_active_star=10000, compact_bulk=0,
                               ms_per_step=ms, bulk_iters=sum(s["bulk_iters"] for s in st),
                               Mcell_steps_per_s=wl.cell_steps / ms / 1e3, note="paper: bulk over all cells")),
               flush=True)
-        chem.set_opts(kmax_bulk=5, n_active_star=10000, compact_bulk=1)
+        chem.set_opts(kmax_bulk=5, n_active_star=-1, compact_bulk=1, schedule_lpt=2)
         del wl
         torch.cuda.empty_cache()
     if args.no_fusion:
