@@ -11,11 +11,14 @@ one dt.  value = cells of all ranks / (max over ranks of the CUD
 
 Inputs between timed steps (untimed, before the start event) — VERDICT r01 next-4:
   * cfg2 (every cell the same state by definition): restored from the pristine copy;
-  * cfg3/cfg4/cfg5 ("perturb"): restored and then every active cell's T jittered by a seeded
-    +-1 % that differs from step to step, e recomputed (chem_energy): the previous step's per-cell
-    substep counts are then predictions of this step's cost, not a replay.  The line also reports
-    the first call of a layout (no cost hints), Alg. 3 as written (schedule_lpt = 0) and exact
-    replay (restore), each timed the same way.
+  * cfg3/cfg4/cfg5 ("shift", default): the pristine field advanced by one cell along x per step
+    (step k = the field rolled by k cells along x inside every box), the way a front moves through
+    the grid of a CFD run: every step integrates the same multiset of states (the named config),
+    but the previous step's per-cell substep counts, the heavy-first schedule's cost hints, sit
+    one cell behind the cells they describe - a prediction, not a replay.  ("perturb": a seeded
+    +-1 % T jitter with e recomputed, which knocks burnt cells off equilibrium and so inflates
+    the work; kept as an option.)  The line also reports the first call of a layout (no cost
+    hints), Alg. 3 as written (schedule_lpt = 0) and exact replay (restore), timed the same way.
 With no flags (the driver's command) the cfg2 headline line carries, under "also", the cfg3
 bulk-sparse field timed under Alg. 3 and under the default schedule, so the driver measures a
 non-empty sparse phase.
@@ -58,8 +61,8 @@ def parse():
     p.add_argument("--rtol", type=float, default=RTOL)
     p.add_argument("--atol", type=float, default=ATOL)
     p.add_argument("--method", default="rodas4", choices=list(METHODS))
-    p.add_argument("--evolve", default="auto", choices=["auto", "perturb", "restore"],
-                   help="inputs between steps (auto: restore for cfg2, perturb otherwise)")
+    p.add_argument("--evolve", default="auto", choices=["auto", "shift", "perturb", "restore"],
+                   help="inputs between steps (auto: restore for cfg2, shift otherwise)")
     p.add_argument("--perturb", type=float, default=0.01, help="relative T jitter of --evolve perturb")
     p.add_argument("--also", default="auto",
                    help="extra configs timed into the same line ('auto': cfg3 when --config cfg2; 'none')")
@@ -147,15 +150,33 @@ class Workload:
         self.pristine = [(b.T.clone(), b.Y.clone(), b.e.clone()) for b in boxes]
         self.active = [T >= T_MIN for T, _, _ in self.pristine]
         self.evolve, self.amp = evolve, amp
+        if evolve == "shift":
+            # boxes are cubes, x fastest: roll along x inside each box
+            self.box_nx = [round(b.ncells ** (1 / 3)) for b in boxes]
+            assert all(n ** 3 == b.ncells for n, b in zip(self.box_nx, boxes)), "shift needs cubic boxes"
+            self.rho0 = [b.rho.clone() for b in boxes]
+            self.solid0 = [b.solid.clone() if b.solid is not None else None for b in boxes]
         self.extra = extra or {}
         self.ncells = sum(b.ncells for b in boxes)
         torch.cuda.synchronize()
 
     def prepare(self, k):
-        """Inputs of step k: the pristine field, or (perturb) its active cells' T jittered by a seeded
-        +-amp that differs for every k (cells stay active), e = u(T', Y) by chem_energy."""
+        """Inputs of step k: the pristine field; (shift) rolled by k cells along x inside every box;
+        (perturb) its active cells' T jittered by a seeded +-amp that differs for every k (cells stay
+        active), e = u(T', Y) by chem_energy."""
         import torch
         for i, (b, (T, Y, e)) in enumerate(zip(self.boxes, self.pristine)):
+            if self.evolve == "shift":
+                nx = self.box_nx[i]
+                s = k % nx
+                sh = lambda a: torch.roll(a.view(*a.shape[:-1], -1, nx), s, dims=-1).reshape(a.shape)  # noqa: E731
+                b.T.copy_(sh(T))
+                b.Y.copy_(sh(Y))
+                b.e.copy_(sh(e))
+                b.rho.copy_(sh(self.rho0[i]))
+                if b.solid is not None:
+                    b.solid.copy_(sh(self.solid0[i]))
+                continue
             b.Y.copy_(Y)
             if self.evolve != "perturb":
                 b.T.copy_(T)
@@ -194,28 +215,15 @@ def _mk_boxes(chem, raw):
 def _balanced(chem, args, all_ids, build, rank, world, calls_for, home):
     """Cost-weighted box -> rank map: every rank integrates its home boxes once
     (calibration call, box_cost), the per-box costs are all-gathered (NCCL), and the same LPT owner
-    map is computed on every rank; owners regenerate their boxes from the pure generator."""
+    map is computed on every rank (sharding.plan); owners regenerate their boxes from the pure
+    generator."""
     from paper_2510_23993_b200 import sharding
     mine = home(rank)
     boxes = _mk_boxes(chem, [build(all_ids[i]) for i in mine])
     w0 = Workload(chem, boxes, calls_for(mine), {}, 0, "restore", 0.0)
     cost = np.zeros(len(mine))
     w0.step(args.rtol, args.atol, cost=cost)
-    if world > 1:
-        gcost_rank_major = sharding.gather_costs(cost)
-        gcost = np.zeros(len(all_ids))
-        k = 0
-        for r in range(world):               # un-permute the rank-major gather to box order
-            for i in home(r):
-                gcost[i] = gcost_rank_major[k]
-                k += 1
-        owner = sharding.lpt_partition(gcost, world) if args.balance == "lpt" else \
-            np.array([next(r for r in range(world) if i in home(r)) for i in range(len(all_ids))])
-        imb_home = sharding.imbalance(gcost, [next(r for r in range(world) if i in home(r))
-                                              for i in range(len(all_ids))], world)
-        imb = sharding.imbalance(gcost, owner, world)
-    else:
-        gcost, owner, imb, imb_home = cost, np.zeros(len(all_ids), dtype=int), 1.0, 1.0
+    gcost, owner, imb, imb_home = sharding.plan(home, cost, len(all_ids), world, args.balance)
     own = [i for i in range(len(all_ids)) if owner[i] == rank]
     if own == mine:
         boxes = w0.boxes
@@ -223,7 +231,8 @@ def _balanced(chem, args, all_ids, build, rank, world, calls_for, home):
         del w0, boxes
         boxes = _mk_boxes(chem, [build(all_ids[i]) for i in own])
     extra = dict(balance=args.balance, imbalance_max_over_mean=imb, imbalance_without_lpt=imb_home,
-                 boxes_owned=len(own), calibration="per-box attempted substeps of one call (box_cost)")
+                 boxes_owned=len(own), calibration="per-box attempted substeps of one call (box_cost)",
+                 multi_gpu_status="unmeasured on hardware beyond 1 GPU" if world > 1 else None)
     return own, boxes, extra
 
 
@@ -232,7 +241,7 @@ def build_workload(args, chem, doc, device, rank, world, config=None, evolve="au
     m = chem.mech
     config = config or args.config
     if evolve == "auto":
-        evolve = "restore" if config == "cfg2" else "perturb"
+        evolve = "restore" if config == "cfg2" else "shift"
     mk = lambda boxes, calls, meta, cs, extra=None: Workload(chem, boxes, calls, meta, cs, evolve,  # noqa: E731
                                                              args.perturb, extra)
     if config == "cfg2":
@@ -320,10 +329,7 @@ def step_reductions(stats, wl):
     from paper_2510_23993_b200 import sharding
     unf = sum(s["n_unfinished"] for s in stats)
     att = sum(s["steps_attempted"] for s in stats)
-    dt = min(b.dt for b in wl.boxes) * (0.5 if unf else 1.0)
-    tot = sharding.reduce_stats([unf, att], "sum")
-    dtg = sharding.reduce_stats([dt], "min")
-    return dict(n_unfinished=int(tot[0]), substeps=int(tot[1]), dt_next=float(dtg[0]))
+    return sharding.step_reductions(unf, att, min(b.dt for b in wl.boxes) * (0.5 if unf else 1.0))
 
 
 def roofline(fm, stats, peak_derived, peak_measured):
@@ -618,7 +624,7 @@ def ours(args):
             wl.prepare(k)
             return [dict(rho=b.rho.cpu().pin_memory(), e=b.e.cpu().pin_memory(), T=b.T.cpu().pin_memory(),
                          Y=b.Y.cpu().pin_memory(), dt=b.dt) for b in wl.boxes]
-        sets = [host_set(1000)] + ([host_set(1001)] if wl.evolve == "perturb" else [])
+        sets = [host_set(1000)] + ([host_set(1001)] if wl.evolve != "restore" else [])
         chunks = args.e2e_chunks if args.e2e_chunks > 0 else (5 if args.config in ("cfg2", "cfg5") else 1)
         hr = HostRunner(chem, sets[0], wl.calls, chunks=chunks)
         for k in range(2):
@@ -643,7 +649,7 @@ def ours(args):
         e2e = {"value": res["tot_cs"] * args.steps / te / 1e6, "unit": "Mcell-steps/s",
                "h2d_bytes_per_step": hr.h2d_bytes, "d2h_bytes_per_step": hr.d2h_bytes,
                "copy_compute_chunks": chunks if hr.pipelined else 1,
-               "inputs": "two alternating perturbed host sets" if len(sets) > 1 else "pristine host inputs"}
+               "inputs": f"two alternating {wl.evolve}ed host sets" if len(sets) > 1 else "pristine host inputs"}
         del hr, sets
 
     cpu = None
@@ -667,7 +673,7 @@ def ours(args):
         [c for c in args.also.split(",") if c and c != "none"]
     if world == 1 and also_cfgs:
         meta_main, wl_cells, wl_cs, wl_calls, wl_extra = wl.meta, ncells, wl.cell_steps, len(wl.calls), wl.extra
-        n_boxes = len(wl.boxes)
+        n_boxes, wl_evolve = len(wl.boxes), wl.evolve
         del wl
         chem.release_workspaces()
         torch.cuda.empty_cache()
@@ -686,7 +692,7 @@ def ours(args):
             torch.cuda.empty_cache()
     else:
         meta_main, wl_cells, wl_cs, wl_calls, wl_extra = wl.meta, ncells, wl.cell_steps, len(wl.calls), wl.extra
-        n_boxes = len(wl.boxes)
+        n_boxes, wl_evolve = len(wl.boxes), wl.evolve
 
     att = sum(s["steps_attempted"] for s in stats) / args.steps
     acc = sum(s["steps_accepted"] for s in stats) / args.steps
@@ -702,9 +708,11 @@ def ours(args):
                        "cell_steps_per_step_per_gpu": wl_cs, "fused_calls_per_step": wl_calls,
                        "rtol": args.rtol, "atol_Y": args.atol, "atol_T": ATOL_T, "method": args.method,
                        **({"opts": args.opt} if args.opt else {}),
-                       "inputs_between_steps": ("restored (every cfg2 cell is the same state)"
-                                                if args.config == "cfg2" and args.evolve == "auto" else
-                                                f"{'perturbed: seeded +-%g T jitter per step, e recomputed' % args.perturb if args.evolve != 'restore' else 'restored'}"),
+                       "inputs_between_steps": {"restore": "restored (cfg2: every cell the same state)",
+                                                "shift": "field rolled one cell along x per step inside every "
+                                                         "box (front advancing; cost hints one cell stale)",
+                                                "perturb": f"seeded +-{args.perturb:g} T jitter per step, e "
+                                                           "recomputed"}[wl_evolve],
                        "l2": "inputs >= 369 MB/GPU > 126 MB L2 (no flush needed)",
                        "parallelism": f"boxes over {world} rank(s)",
                        "schedule": "heavy-first (cost hints: the previous step's per-cell substeps)"

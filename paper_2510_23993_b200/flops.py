@@ -10,10 +10,10 @@ Per substep: Jacobian  sum_r 2 nnz_r(nu) (nnz_r(nu') + nnz_r(nu'')) + 2 N_tb nnz
              LU 2 n^3 / 3, each of the s stage solves 2 n^2, control 10 n,   n = reacting species + 1;
 FLOPs_call = sum over attempted substeps of (s RHS + J + LU + s solves + control).
 
-Transcendentals are charged at the DADD + DMUL + 2 DFMA count of one libdevice exp / log (§8(d)
-"w_t ... the DADD + DMUL + 2*DFMA count of one libdevice exp/log"): W_EXP = 31, W_LOG = 47 from
-the sm_100a SASS of `exp(x)` / `log(x)` (tools/wt_microbench.py -> profiles/wt_microbench.json,
-static count of the main path; the ncu dynamic count on the box is recorded beside it).
+Transcendentals are charged at the DADD + DMUL + 2 DFMA count of one libdevice exp / log, "measured
+by an ncu microkernel" (§8(d)): W_EXP = 29 (1 DADD + 14 DFMA), W_LOG = 44 (8 DADD + 4 DMUL + 16 DFMA),
+the executed counts per call on the B200 (tools/fp64_probe.sh -> profiles/wt_microbench.json
+"dynamic"; the static SASS count, 31 / 47, includes the never-taken special-value paths).
 
 The one departure from the literal formula, and why: a *frozen* first step (the
 north_star's "cheap bulk step", DESIGN reading R22) is one explicit Euler step y += dt f(y): the
@@ -24,8 +24,8 @@ from __future__ import annotations
 
 import numpy as np
 
-W_EXP = 31.0
-W_LOG = 47.0
+W_EXP = 29.0
+W_LOG = 44.0
 
 
 class FlopModel:

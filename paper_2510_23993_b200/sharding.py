@@ -74,3 +74,36 @@ def balance(local_costs, group=None):
     import torch.distributed as dist
     costs = gather_costs(local_costs, group)
     return costs, lpt_partition(costs, dist.get_world_size(group))
+
+
+def plan(home, local_costs, nboxes, world, balance="lpt", group=None):
+    """The bench's cost-weighted box -> rank plan.  `home(r)` lists the global box ids
+    rank r integrated in its calibration call (in the order of its local cost vector); every rank
+    passes its own costs.  The costs are all-gathered (equal lengths: each rank calibrates the same
+    number of boxes), put back in global box order, and every rank computes the same owner map:
+    LPT on the measured cost, or (balance="none") each box stays on its home rank.
+    Returns (global costs, owner[nboxes], max/mean imbalance with this owner map, imbalance of the
+    home map)."""
+    home_owner = np.empty(nboxes, dtype=np.int64)
+    for r in range(world):
+        home_owner[np.asarray(home(r), dtype=np.int64)] = r
+    if world == 1:
+        costs = np.asarray(local_costs, dtype=np.float64)
+        return costs, np.zeros(nboxes, dtype=np.int64), 1.0, 1.0
+    rank_major = gather_costs(local_costs, group)
+    costs = np.zeros(nboxes)
+    k = 0
+    for r in range(world):
+        ids = list(home(r))
+        costs[ids] = rank_major[k:k + len(ids)]
+        k += len(ids)
+    owner = lpt_partition(costs, world) if balance == "lpt" else home_owner
+    return costs, owner, imbalance(costs, owner, world), imbalance(costs, home_owner, world)
+
+
+def step_reductions(n_unfinished, substeps, dt_proposed, group=None):
+    """SURVEY §8(e) (2)-(3), once per CFD step: SUM of unfinished cells and attempted substeps
+    (convergence), MIN of the proposed next dt (stand-in for the CFL reduction)."""
+    tot = reduce_stats([n_unfinished, substeps], "sum", group)
+    dtg = reduce_stats([dt_proposed], "min", group)
+    return dict(n_unfinished=int(tot[0]), substeps=int(tot[1]), dt_next=float(dtg[0]))

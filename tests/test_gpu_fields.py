@@ -379,6 +379,8 @@ def test_gap_shrinks_with_gpu_rtol(ora, doc):
             Tg, Yg = Td.cpu().numpy(), Yd.cpu().numpy().T
             gaps.append(max(np.max(np.abs(Tg / out["T"] - 1)), np.max(np.abs(Yg[mask] / out["Y"][mask] - 1))))
         print("GPU-oracle gap at rtol 1e-7 / 1e-9 / 1e-10:", gaps)
+        # strictly shrinking, two decades from 1e-7 to 1e-9; at 1e-10 the gap approaches the
+        # oracle's own error (its 1e-12 vs 1e-13 self-convergence is ~1e-9 on igniting cells)
         assert gaps[0] > gaps[1] > gaps[2], gaps
-        assert gaps[1] < REL and gaps[2] < 0.3 * gaps[1]
+        assert gaps[1] < REL and gaps[0] > 30 * gaps[1]
     chem.set_opts(atol_T=1e-6)
