@@ -150,12 +150,12 @@ class Workload:
         self.pristine = [(b.T.clone(), b.Y.clone(), b.e.clone()) for b in boxes]
         self.active = [T >= T_MIN for T, _, _ in self.pristine]
         self.evolve, self.amp = evolve, amp
+        self.rho0 = [b.rho.clone() for b in boxes]
+        self.solid0 = [b.solid.clone() if b.solid is not None else None for b in boxes]
         if evolve == "shift":
             # boxes are cubes, x fastest: roll along x inside each box
             self.box_nx = [round(b.ncells ** (1 / 3)) for b in boxes]
             assert all(n ** 3 == b.ncells for n, b in zip(self.box_nx, boxes)), "shift needs cubic boxes"
-            self.rho0 = [b.rho.clone() for b in boxes]
-            self.solid0 = [b.solid.clone() if b.solid is not None else None for b in boxes]
         self.extra = extra or {}
         self.ncells = sum(b.ncells for b in boxes)
         torch.cuda.synchronize()
@@ -178,6 +178,9 @@ class Workload:
                     b.solid.copy_(sh(self.solid0[i]))
                 continue
             b.Y.copy_(Y)
+            b.rho.copy_(self.rho0[i])               # a shift step may have rolled rho / solid
+            if b.solid is not None:
+                b.solid.copy_(self.solid0[i])
             if self.evolve != "perturb":
                 b.T.copy_(T)
                 b.e.copy_(e)
@@ -544,7 +547,7 @@ def measure(args, chem, doc, device, rank, world, dist, config, fm, peaks, with_
             var[name] = dict(value=tot_cs * n / t / 1e6, ms_per_step=1e3 * t / n, steps=n,
                              frac=a / peaks[0], lpt=s0.get("lpt", 0), lockstep=s0["lockstep"],
                              bulk_iters=s0["bulk_iters"], sparse_cells=s0["sparse_cells"],
-                             t_sparse_ms=s0["t_sparse_ms"])
+                             t_sparse_ms=s0["t_sparse_ms"], hint_accuracy=s0.get("hint_accuracy"))
         res["schedules"] = var
     if with_variants and not args.no_prod:
         # SURVEY §8(d) secondary number: production tolerance (rtol 1e-6, atol_Y 1e-12, atol_T 1e-3 K)
@@ -684,6 +687,7 @@ def ours(args):
             also.append(dict(config=c, workload=w2.meta["workload"], schedule="default (heavy-first when the "
                              "previous step's hints are skewed)", inputs=w2.evolve, value=r2["value"],
                              ms_per_step=r2["ms_per_step"], frac=r2["achieved"] / peak, lpt=s0.get("lpt", 0),
+                             hint_accuracy=s0.get("hint_accuracy"),
                              sparse_cells=s0["sparse_cells"], bulk_iters=s0["bulk_iters"],
                              substeps_per_cell_step=sum(s["steps_attempted"] for s in r2["stats"]) / args.steps
                              / max(w2.cell_steps, 1), schedules=r2.get("schedules")))
@@ -741,6 +745,7 @@ def ours(args):
                        "t_sparse_ms": s0["t_sparse_ms"], "n_unfinished": s0["n_unfinished"],
                        "n_nonfinite": s0["n_nonfinite"], "max_energy_drift": s0["max_energy_drift"],
                        "lockstep": s0["lockstep"], "lpt": s0.get("lpt", 0),
+                       "hint_accuracy": s0.get("hint_accuracy"),
                        "bulk_simt_eff": s0["bulk_substeps"] / max(32 * s0["warp_substeps"], 1),
                        "step_reductions": res["reductions"]},
         }

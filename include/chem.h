@@ -109,8 +109,9 @@ typedef struct {
                                per-cell substeps (kept in the workspace; used only when this call
                                integrates the same cell layout) and run as one persistent lockstep
                                launch, longest cells first: 0 off, 1 on, 2 auto (on when the hints
-                               are skewed: cells above 64 substeps carried half of the previous call's
-                               work, or the largest hint exceeds 1.5x the mean).  Bitwise-neutral.  */
+                               are skewed - cells above 64 substeps carried half of the previous call's
+                               work, or the largest hint exceeds 1.5x the mean - and predictive: the
+                               layout's last chem_stats.hint_accuracy >= 0.9).  Bitwise-neutral.   */
 } chem_opts;
 
 /* fills the defaults: T_min 500 K, kmax_bulk 5, n_active_star -1 (auto: one resident wave),
@@ -157,6 +158,10 @@ typedef struct {
     int64_t bulk_substeps;      /* lane substeps attempted in bulk launches                     */
     int64_t lockstep;           /* 1: this call's bulk bursts ran in lockstep                   */
     int64_t lpt;                /* 1: this call ran the heavy-first schedule (schedule_lpt)        */
+    double hint_accuracy;       /* how well the cost hints (the previous call's per-cell substeps on
+                                   this layout) predicted this call: sum_cells min(hint, actual) /
+                                   sum_cells max(hint, actual); -1 without hints.  schedule_lpt = 2
+                                   engages heavy-first only while the last value is >= 0.9        */
 } chem_stats;
 
 typedef struct chem_ctx chem_ctx;   /* opaque, library-owned */

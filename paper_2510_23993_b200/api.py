@@ -30,13 +30,13 @@ def _check(t, name, dtype=torch.float64, n=None, device=None):
     if device is not None and t.device != device:
         raise ValueError(f"{name} is on {t.device}, the ctx on {device}")
     if n is not None:
-        if t.dim() != 1 or t.stride(0) != 1 or t.numel() < n:
+        if t.dim() != 1 or (t.numel() > 1 and t.stride(0) != 1) or t.numel() < n:
             raise ValueError(f"{name} must be a contiguous 1-D tensor of >= {n} elements")
 
 
 def _species(Y, ns, n=None):
     _check(Y, "Y")
-    if Y.dim() != 2 or Y.shape[0] != ns or Y.stride(1) != 1:
+    if Y.dim() != 2 or Y.shape[0] != ns or (Y.shape[1] > 1 and Y.stride(1) != 1):
         raise ValueError(f"Y must be [ns={ns}, ld] with unit stride along cells")
     if n is not None and Y.shape[1] < n:
         raise ValueError(f"Y has {Y.shape[1]} cells, the call {n}")

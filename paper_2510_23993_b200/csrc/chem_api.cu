@@ -20,6 +20,8 @@ using namespace chem;
 namespace {
 
 constexpr double kLockEff = 0.9;   // chem_opts.lockstep = 2: lockstep while the last bulk SIMT efficiency < 0.9
+constexpr double kHintAcc = 0.9;   // chem_opts.schedule_lpt = 2: heavy-first only while the layout's hints
+                                   // predicted the last call's per-cell substeps this well (sum min/max)
 constexpr int kStreamBS = 256;     // gate / compaction / box cost
 constexpr int kPointBS = 128;      // point kernels
 
@@ -274,7 +276,7 @@ int validate(const chem_mech_desc* d)
 
 // ------------------------------------------------------------------ workspace layout
 struct WsLayout {
-    size_t stats, boxes, start, cell_t, cell_h, steps, box, state, ids0, idsA, idsB, key0, key1, total;
+    size_t stats, boxes, start, cell_t, cell_h, steps, box, hint, state, ids0, idsA, idsB, key0, key1, total;
 };
 
 inline size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -290,6 +292,7 @@ WsLayout ws_layout(int64_t N, int32_t B)
     w.cell_h = o; o = al256(o + (size_t)N * 8);
     w.steps = o; o = al256(o + (size_t)N * 4);
     w.box = o; o = al256(o + (size_t)N * 4);
+    w.hint = o; o = al256(o + (size_t)N * 4);
     w.state = o; o = al256(o + (size_t)N);
     w.ids0 = o; o = al256(o + (size_t)N * 4);
     w.idsA = o; o = al256(o + (size_t)N * 4);
@@ -320,7 +323,7 @@ struct chem_ctx {
     double simt_eff = 1.0;           // bulk SIMT efficiency of the last call (lockstep = 2 input)
     void* sort_tmp = nullptr;        // cub radix-sort scratch of the heavy-first schedule (library-owned)
     size_t sort_tmp_bytes = 0;
-    unsigned long long* h_sig = nullptr;   // pinned [3]: staging of the workspace layout signature
+    unsigned long long* h_sig = nullptr;   // pinned [6]: staging of the signature + hint-accuracy slots
     struct WsRecord { const void* ws; int64_t total; int32_t nboxes; };
     std::vector<WsRecord> ws_last;   // layout of the last call on each workspace (chem_cell_status)
 };
@@ -425,7 +428,7 @@ int chem_init(const chem_mech_desc* mech, const chem_opts* opts, int device, che
     ops->fill(mech, c->params.data());
     cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
     if (cudaMallocHost(&c->h_stats, sizeof(unsigned long long) * S_NSTATS) != cudaSuccess ||
-        cudaMallocHost(&c->h_sig, sizeof(unsigned long long) * 3) != cudaSuccess ||
+        cudaMallocHost(&c->h_sig, sizeof(unsigned long long) * 6) != cudaSuccess ||
         cudaEventCreate(&c->ev[0]) != cudaSuccess || cudaEventCreate(&c->ev[1]) != cudaSuccess ||
         ensure_host_boxes(c, 64) != CHEM_OK) {
         chem_finalize(c);
@@ -611,6 +614,7 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
     L.state = reinterpret_cast<uint8_t*>(base + W.state);
     L.cell_steps = reinterpret_cast<int32_t*>(base + W.steps);
     L.cell_box = reinterpret_cast<int32_t*>(base + W.box);
+    L.cell_hint = reinterpret_cast<int32_t*>(base + W.hint);
     L.stats = reinterpret_cast<unsigned long long*>(base + W.stats);
     L.rtol = rtol;
     L.atol = atol;
@@ -684,8 +688,16 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
     const unsigned long long sig[3] = {(unsigned long long)total, (unsigned long long)nboxes,
                                        (unsigned long long)(uintptr_t)boxes[0].rho};
     const bool history = c->h_stats[S_SIG0] == sig[0] && c->h_stats[S_SIG1] == sig[1] && c->h_stats[S_SIG2] == sig[2];
+    // hint accuracy of this layout's previous call (sum min / sum max of hint vs actual substeps over
+    // its cells), valid if that call had hints of its own; then reset the slots for this call
+    const bool acc_known = history && c->h_stats[S_HINT_VALID] == 1 && c->h_stats[S_HINT_MAX] > 0;
+    const double acc_prev = acc_known ? (double)c->h_stats[S_HINT_MIN] / (double)c->h_stats[S_HINT_MAX] : -1.0;
     std::memcpy(c->h_sig, sig, sizeof(sig));
-    CK(cudaMemcpyAsync(L.stats + S_SIG0, c->h_sig, sizeof(sig), cudaMemcpyHostToDevice, s));
+    c->h_sig[3] = 0;
+    c->h_sig[4] = 0;
+    c->h_sig[5] = history ? 1 : 0;
+    static_assert(S_HINT_MIN == S_SIG2 + 1 && S_HINT_VALID == S_SIG2 + 3, "signature + hint slots are contiguous");
+    CK(cudaMemcpyAsync(L.stats + S_SIG0, c->h_sig, 6 * sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
     const uint64_t pred_total = c->h_stats[S_PRED_TOTAL], pred_heavy = c->h_stats[S_PRED_HEAVY];
     const uint64_t pred_max = c->h_stats[S_PRED_MAX];
     const bool sortable = n_active > 0 && n_active <= (int64_t)0x7fffffff;   // cub's int item count
@@ -694,7 +706,9 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
     const bool skewed = history && pred_total > 0 &&
                         (2 * pred_heavy >= pred_total ||
                          (double)pred_max * (double)n_active > 1.5 * (double)pred_total);
-    const bool lpt = eligible && (o.schedule_lpt == 1 || (o.schedule_lpt == 2 && skewed));
+    // auto: skewed hints that have been predictive (or whose predictiveness is not known yet)
+    const bool lpt = eligible && (o.schedule_lpt == 1 ||
+                                  (o.schedule_lpt == 2 && skewed && (!acc_known || acc_prev >= kHintAcc)));
     st.lpt = lpt ? 1 : 0;
     const uint32_t* cur = ids0;
     int64_t n_cur = n_active;
@@ -805,6 +819,7 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
     st.n_nonfinite = (int64_t)hs[S_NONFINITE];
     st.n_T_range = (int64_t)hs[S_TRANGE];
     st.n_unfinished = (int64_t)hs[S_UNFINISHED];
+    st.hint_accuracy = (history && hs[S_HINT_MAX] > 0) ? (double)hs[S_HINT_MIN] / (double)hs[S_HINT_MAX] : -1.0;
     unsigned long long db = hs[S_DRIFT_BITS];
     std::memcpy(&st.max_energy_drift, &db, 8);
     if (stats) *stats = st;

@@ -30,6 +30,8 @@ enum StatIdx {
     S_DONE, S_DRIFT_BITS, S_COUNT_ACTIVE, S_CURSOR, S_FROZEN, S_WARP_SUBSTEPS, S_PRED_TOTAL, S_PRED_HEAVY,
     S_PRED_MAX,
     S_SIG0, S_SIG1, S_SIG2,   // cell-layout signature of the workspace's cost hints (not cleared per call)
+    S_HINT_MIN, S_HINT_MAX,   // sum over finished cells of min / max(hint, actual substeps): hint accuracy
+    S_HINT_VALID,             // 1 if those sums describe valid hints (the call had the layout's history)
     S_NSTATS
 };
 
@@ -54,6 +56,8 @@ struct LaunchCtx {
     int32_t* cell_steps;       // [total] attempted substeps summed over launches
     int32_t* cell_box;         // [total] box of each active cell (written by the gate: one coalesced
                                // load in load_cell instead of a dependent-load binary search)
+    int32_t* cell_hint;        // [total] the previous call's substeps of the cell (its cost hint),
+                               // compared with the actual count at write-back (hint accuracy)
     unsigned long long* stats; // [S_NSTATS]
     double rtol, atol, atolT, T_min;
     double eps_change;          // explicit scheme: max fractional change per step
@@ -131,7 +135,10 @@ __global__ void __launch_bounds__(BS) k_gate(LaunchCtx L, uint32_t* ids_out, uin
             L.state[g] = act ? ST_FRESH : ST_INACTIVE;
             if (keys_out) prev = act ? (uint32_t)max(L.cell_steps[g], 0) : 0u;
             L.cell_steps[g] = 0;
-            if (act) L.cell_box[g] = b;
+            if (act) {
+                L.cell_box[g] = b;
+                L.cell_hint[g] = (int32_t)prev;
+            }
         }
         if (keys_out) {
             warp_add(&L.stats[S_PRED_TOTAL], prev);
@@ -221,7 +228,7 @@ struct SmemLayout {
 
 struct Counters {
     unsigned attempted = 0, accepted = 0, rhs = 0, newton_fail = 0, nonfinite = 0, trange = 0, unfinished = 0,
-             done = 0, frozen = 0, warp_substeps = 0;
+             done = 0, frozen = 0, warp_substeps = 0, hint_min = 0, hint_max = 0;
     double drift = 0.0;
 };
 
@@ -582,7 +589,12 @@ __device__ __forceinline__ void store_cell(const Params<M>& P, const LaunchCtx& 
     L.cell_t[C.g] = C.t;
     L.cell_h[C.g] = C.h;
     L.state[C.g] = st | (C.rej ? 0x80 : 0);
-    L.cell_steps[C.g] += C.k;
+    L.cell_steps[C.g] = C.kprev + C.k;
+    if (st != ST_RUNNING) {   // the cell's call is over: how well did its hint predict it?
+        const unsigned act = (unsigned)(C.kprev + C.k), hint = (unsigned)L.cell_hint[C.g];
+        cnt.hint_min += min(act, hint);
+        cnt.hint_max += max(act, hint);
+    }
 }
 
 __device__ __forceinline__ void flush_counters(const LaunchCtx& L, Counters& c)
@@ -599,6 +611,8 @@ __device__ __forceinline__ void flush_counters(const LaunchCtx& L, Counters& c)
     warp_add(&L.stats[S_TRANGE], c.trange);
     warp_add(&L.stats[S_UNFINISHED], c.unfinished);
     warp_add(&L.stats[S_DONE], c.done);
+    warp_add(&L.stats[S_HINT_MIN], c.hint_min);
+    warp_add(&L.stats[S_HINT_MAX], c.hint_max);
     // max drift: non-negative doubles order like their bit patterns
     unsigned long long bits = __double_as_longlong(c.drift);
 #pragma unroll
