@@ -50,7 +50,9 @@ def up_to_date() -> bool:
 
 
 def _compile(src: pathlib.Path, obj: pathlib.Path):
-    cmd = [nvcc(), *NVCC_FLAGS, "-c", "-o", str(obj), str(src)]
+    # CHEM_NVCC_EXTRA: extra flags for a kernel experiment (e.g. -DCHEM_...); the default build has none
+    extra = os.environ.get("CHEM_NVCC_EXTRA", "").split()
+    cmd = [nvcc(), *NVCC_FLAGS, *extra, "-c", "-o", str(obj), str(src)]
     r = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
     return src, cmd, r
 
