@@ -62,9 +62,6 @@ struct MechOps {
     static bool match(const chem_mech_desc* d)
     {
         if (d->ns != M::NS || d->nr != M::NR) return false;
-        if (M::kTmidCommon)
-            for (int k = 0; k < M::NS; ++k)
-                if (d->T_range[3 * k + 1] != M::kTmid) return false;
         for (int r = 0; r < M::NR; ++r) {
             if (d->type[r] != M::kind(r) || (d->reversible[r] != 0) != (M::rev(r) != 0)) return false;
             for (int k = 0; k < M::NS; ++k) {
