@@ -61,6 +61,9 @@ def parse():
     p.add_argument("--rtol", type=float, default=RTOL)
     p.add_argument("--atol", type=float, default=ATOL)
     p.add_argument("--method", default="rodas4", choices=list(METHODS))
+    p.add_argument("--mech", default="h2air_li2004",
+                   help="mechanism (mech/<name>.yaml); fields of the 9 H2-air species are mapped by name, "
+                        "NO at 100 ppm by mass replacing N2 when the mechanism has it (NEXT-3)")
     p.add_argument("--evolve", default="auto", choices=["auto", "shift", "perturb", "restore"],
                    help="inputs between steps (auto: restore for cfg2, shift otherwise)")
     p.add_argument("--perturb", type=float, default=0.01, help="relative T jitter of --evolve perturb")
@@ -206,9 +209,30 @@ class Workload:
         return stats
 
 
+def _map_species(chem, raw):
+    """Expand 9-species H2-air boxes to the ctx's mechanism by species name (NEXT-3 mechanisms)."""
+    import torch
+    import synth
+    src = synth.load_trajectories()["species"]
+    dst = chem.mech.species
+    if list(dst) == list(src):
+        return raw
+    for b in raw:
+        Y = torch.zeros((len(dst), b["Y"].shape[1]), dtype=b["Y"].dtype, device=b["Y"].device)
+        for j, s in enumerate(src):
+            Y[dst.index(s)] = b["Y"][j]
+        if "NO" in dst:
+            no = 1e-4 * Y[dst.index("N2")]
+            Y[dst.index("NO")] += no
+            Y[dst.index("N2")] -= no
+        b["Y"] = Y
+    return raw
+
+
 def _mk_boxes(chem, raw):
     from paper_2510_23993_b200 import Box
     out = []
+    raw = _map_species(chem, raw)
     for b in raw:
         e = chem.energy(b["T"], b["Y"])            # e = u(T0, Y) with the CUDA path's own thermo
         out.append(Box(b["rho"], e, b["T"].clone(), b["Y"].clone(), b["dt"], b.get("solid")))
@@ -434,7 +458,7 @@ def oracle_stratified(chem, wl, rtol, atol, seconds_target, n_prop=65536, n_heav
     class count) and LABELLED an extrapolation.  A sub-sample is also timed on one core."""
     import torch
     from oracle import Oracle
-    o = Oracle("h2air_li2004")
+    o = Oracle(chem.mech.name)
     wl.prepare(0)
     # pristine inputs (the named config), one GPU call for the per-cell substep counts
     for b, (T, Y, e) in zip(wl.boxes, wl.pristine):
@@ -590,7 +614,7 @@ def ours(args):
             dist.init_process_group("gloo")
     pg = dist if world > 1 else None
     method = METHODS[args.method]
-    chem = Chem("h2air_li2004", device=local, atol_T=ATOL_T, method=method, **_opts(args))
+    chem = Chem(args.mech, device=local, atol_T=ATOL_T, method=method, **_opts(args))
     doc = synth.load_trajectories()
     fm = FlopModel(chem.mech, stages=STAGES[method])
     sm_mhz_peak = 1965.0
@@ -657,7 +681,7 @@ def ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        if args.config == "cfg2":
+        if args.config == "cfg2" and args.mech == "h2air_li2004":
             r = oracle_sample(wl.meta, args.cpu_sample_seconds, args.rtol, args.atol)
             cpu = {"value": r["value"], "unit": "Mcell-steps/s", "cores": r["threads"], "kind": "oracle",
                    "one_core_value": r["one_core_value"],
@@ -708,7 +732,9 @@ def ours(args):
             "metric": METRIC, "value": res["value"], "unit": "Mcell-steps/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": res["ms_per_step"], "higher_is_better": True,
             "scaling": meta_main.get("scaling", "weak"), "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": meta_main["workload"], "cells_per_gpu": wl_cells, "boxes_per_gpu": n_boxes,
+            "config": {"workload": meta_main["workload"] + ("" if args.mech == "h2air_li2004" else
+                                                            f" [mechanism {args.mech}, {chem.ns} species]"),
+                       "mechanism": args.mech, "cells_per_gpu": wl_cells, "boxes_per_gpu": n_boxes,
                        "cell_steps_per_step_per_gpu": wl_cs, "fused_calls_per_step": wl_calls,
                        "rtol": args.rtol, "atol_Y": args.atol, "atol_T": ATOL_T, "method": args.method,
                        **({"opts": args.opt} if args.opt else {}),
