@@ -265,7 +265,10 @@ def _balanced(chem, args, all_ids, build, rank, world, calls_for, home):
 
 def build_workload(args, chem, doc, device, rank, world, config=None, evolve="auto"):
     import synth
-    m = chem.mech
+    from paper_2510_23993_b200 import mechanism
+    # the field generators and the trajectory table speak the 9 H2-air species; boxes are mapped to
+    # the ctx's mechanism by name afterwards (_map_species)
+    m = chem.mech if chem.mech.name == "h2air_li2004" else mechanism.load("h2air_li2004")
     config = config or args.config
     if evolve == "auto":
         evolve = "restore" if config == "cfg2" else "shift"
