@@ -322,34 +322,39 @@ __device__ __forceinline__ int ros_step(const Params<M>& P, const LaunchCtx& L, 
         for (int s = 1; s < S; ++s) {
             double F[n];
             double ys[n];
-            double G[n];
+            // stage point first; the sum_j c_sj K_j / h term is formed after the RHS from the slots
+            // again, so it is not live across the rate evaluation (register pressure)
             if (s <= 3) {
 #pragma unroll
-                for (int i = 0; i < n; ++i) { ys[i] = C.y[i]; G[i] = 0.0; }
+                for (int i = 0; i < n; ++i) ys[i] = C.y[i];
 #pragma unroll
                 for (int j = 0; j < 3; ++j) {
                     if (j < s) {
-                        const double a = Meth::a_rt(s, j), c = Meth::c_rt(s, j);
+                        const double a = Meth::a_rt(s, j);
 #pragma unroll
-                        for (int i = 0; i < n; ++i) {
-                            const double kj = slot(j)[i * ss];
-                            ys[i] = fma(a, kj, ys[i]);
-                            G[i] = fma(c, kj, G[i]);
-                        }
+                        for (int i = 0; i < n; ++i) ys[i] = fma(a, slot(j)[i * ss], ys[i]);
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < n; ++i) ys[i] = C.y[i] + slot(0)[i * ss];
+            }
+            rhs<M>(P, C.rho, invrho, ys, C.Yin, F);
+            cnt.rhs++;
+            if (s <= 3) {
+#pragma unroll
+                for (int j = 0; j < 3; ++j) {
+                    if (j < s) {
+                        const double c = Meth::c_rt(s, j) * hinv;
+#pragma unroll
+                        for (int i = 0; i < n; ++i) F[i] = fma(c, slot(j)[i * ss], F[i]);
                     }
                 }
             } else {
                 const double* gs = slot(s == 4 ? 1 : 2);
 #pragma unroll
-                for (int i = 0; i < n; ++i) {
-                    ys[i] = C.y[i] + slot(0)[i * ss];
-                    G[i] = gs[i * ss];
-                }
+                for (int i = 0; i < n; ++i) F[i] = fma(hinv, gs[i * ss], F[i]);
             }
-            rhs<M>(P, C.rho, invrho, ys, C.Yin, F);
-            cnt.rhs++;
-#pragma unroll
-            for (int i = 0; i < n; ++i) F[i] = fma(hinv, G[i], F[i]);
             if (s == 3) {
                 // collapse (K_0, K_1, K_2) -> (sum a_4j K_j, sum c_4j K_j, sum c_5j K_j), j < 3
                 const double a0 = Meth::a_rt(4, 0), a1 = Meth::a_rt(4, 1), a2 = Meth::a_rt(4, 2);
