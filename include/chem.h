@@ -105,13 +105,17 @@ typedef struct {
                                bitwise independent of this choice.                                */
     int32_t kmax_first;     /* substeps of the first bulk burst of a lockstep call (1: cells that
                                finish in one substep leave before the lockstep bursts); 0: kmax_bulk */
-    int32_t schedule_lpt;   /* heavy-first schedule: the active list sorted by the previous call's
-                               per-cell substeps (kept in the workspace; used only when this call
-                               integrates the same cell layout) and run as one persistent lockstep
-                               launch, longest cells first: 0 off, 1 on, 2 auto (on when the hints
-                               are skewed - cells above 64 substeps carried half of the previous call's
-                               work, or the largest hint exceeds 1.5x the mean - and predictive: the
-                               layout's last chem_stats.hint_accuracy >= 0.9).  Bitwise-neutral.   */
+    int32_t schedule_lpt;   /* heavy-first schedule: the active list sorted by predicted cost and run as
+                               one persistent lockstep launch, longest cells first.  Predictions come
+                               from the previous call's per-cell substeps on the same layout (kept in
+                               the workspace) or, within the call, from each cell's own state after the
+                               first bulk burst (remaining substeps (dt - t)/h).  0 off (Alg. 3);
+                               1 previous-call hints always; 2 auto: previous-call hints when they are
+                               skewed (cells above 64 substeps carried half of the work, or the largest
+                               hint exceeds 1.5x the mean) and predictive (the layout's last
+                               chem_stats.hint_accuracy >= 0.9), else the in-call prediction when it
+                               is skewed (max > 1.5x mean); 3 in-call prediction always.
+                               Bitwise-neutral.                                                     */
 } chem_opts;
 
 /* fills the defaults: T_min 500 K, kmax_bulk 5, n_active_star -1 (auto: one resident wave),
@@ -157,7 +161,8 @@ typedef struct {
                                    bulk lane substeps / (32 x warp_substeps))                   */
     int64_t bulk_substeps;      /* lane substeps attempted in bulk launches                     */
     int64_t lockstep;           /* 1: this call's bulk bursts ran in lockstep                   */
-    int64_t lpt;                /* 1: this call ran the heavy-first schedule (schedule_lpt)        */
+    int64_t lpt;                /* heavy-first schedule of this call: 0 no, 1 on the previous call's
+                                   hints, 2 on the in-call prediction after the first burst       */
     double hint_accuracy;       /* how well the cost hints (the previous call's per-cell substeps on
                                    this layout) predicted this call: sum_cells min(hint, actual) /
                                    sum_cells max(hint, actual); -1 without hints.  schedule_lpt = 2

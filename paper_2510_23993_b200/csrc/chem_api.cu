@@ -398,7 +398,7 @@ static int check_opts(const chem_opts* o)
     if (o->kmax_bulk < 1 || o->kmax_sparse < 1 || !(o->atol_T > 0.0) ||
         (o->method < CHEM_METHOD_RODAS4 || o->method > CHEM_METHOD_EXPLICIT) ||
         !std::isfinite(o->T_min) || !(o->eps_change > 0.0 && o->eps_change <= 1.0) ||
-        o->lockstep < 0 || o->lockstep > 2 || o->kmax_first < 0 || o->schedule_lpt < 0 || o->schedule_lpt > 2 ||
+        o->lockstep < 0 || o->lockstep > 2 || o->kmax_first < 0 || o->schedule_lpt < 0 || o->schedule_lpt > 3 ||
         !(o->h0_factor > 0.0 && o->h0_factor <= 1.0) || (o->compact_bulk != 0 && o->compact_bulk != 1))
         return CHEM_EINVAL;
     return CHEM_OK;
@@ -707,27 +707,36 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
                         (2 * pred_heavy >= pred_total ||
                          (double)pred_max * (double)n_active > 1.5 * (double)pred_total);
     // auto: skewed hints that have been predictive (or whose predictiveness is not known yet)
-    const bool lpt = eligible && (o.schedule_lpt == 1 ||
-                                  (o.schedule_lpt == 2 && skewed && (!acc_known || acc_prev >= kHintAcc)));
+    bool lpt = eligible && (o.schedule_lpt == 1 ||
+                            (o.schedule_lpt == 2 && skewed && (!acc_known || acc_prev >= kHintAcc)));
+    // otherwise (auto, or schedule_lpt = 3) the cells predict their own cost after the first burst
+    const bool predict = eligible && !lpt && (o.schedule_lpt == 2 || o.schedule_lpt == 3);
     st.lpt = lpt ? 1 : 0;
     const uint32_t* cur = ids0;
     int64_t n_cur = n_active;
     uint32_t* nxt = idsA;
-    if (lpt) {
-        cub::DoubleBuffer<uint32_t> dk(key0, key1), dv(ids0, idsA);
+    // stable descending radix sort of (keys, ids) over the bits in use; returns the sorted id list
+    auto sort_desc = [&](uint32_t* k_a, uint32_t* k_b, uint32_t* v_a, uint32_t* v_b, int64_t n, uint64_t kmax,
+                         const uint32_t*& out) -> cudaError_t {
+        cub::DoubleBuffer<uint32_t> dk(k_a, k_b), dv(v_a, v_b);
         size_t need = 0;
-        int bits = 1;                                    // keys <= pred_max: sort only the bits in use
-        while (bits < 32 && (1ull << bits) <= pred_max) ++bits;
-        CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, need, dk, dv, (int)n_active, 0, bits, s));
+        int bits = 1;
+        while (bits < 32 && (1ull << bits) <= kmax) ++bits;
+        cudaError_t r = cub::DeviceRadixSort::SortPairsDescending(nullptr, need, dk, dv, (int)n, 0, bits, s);
+        if (r != cudaSuccess) return r;
         if (need > c->sort_tmp_bytes) {
-            if (c->sort_tmp) CK(cudaFree(c->sort_tmp));
+            if (c->sort_tmp) cudaFree(c->sort_tmp);
             c->sort_tmp = nullptr;
             c->sort_tmp_bytes = 0;
-            CK(cudaMalloc(&c->sort_tmp, need));
+            if ((r = cudaMalloc(&c->sort_tmp, need)) != cudaSuccess) return r;
             c->sort_tmp_bytes = need;
         }
-        CK(cub::DeviceRadixSort::SortPairsDescending(c->sort_tmp, need, dk, dv, (int)n_active, 0, bits, s));
-        cur = dv.Current();
+        r = cub::DeviceRadixSort::SortPairsDescending(c->sort_tmp, need, dk, dv, (int)n, 0, bits, s);
+        out = dv.Current();
+        return r;
+    };
+    if (lpt) {
+        CK(sort_desc(key0, key1, ids0, idsA, n_active, pred_max, cur));
         nxt = (cur == idsA) ? idsB : idsA;
     }
 
@@ -777,6 +786,24 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
         }
         cur = nxt;
         nxt = (nxt == idsA) ? idsB : idsA;
+        if (predict && st.bulk_iters == 1 && n_cur > nstar) {
+            // heavy-first on in-call predictions: the remaining substeps (dt - t)/h of every cell still
+            // active after the first burst; skewed (max > 1.5 mean) or forced -> sort, one persistent launch
+            CK(cudaMemsetAsync(L.stats + S_PRED2_TOTAL, 0, 16, s));
+            k_predict<kStreamBS><<<grid_for(n_cur, kStreamBS), kStreamBS, 0, s>>>(L, cur, n_cur, key0);
+            CK(cudaGetLastError());
+            int64_t dummy;
+            CK(read_count(dummy));
+            const uint64_t p_tot = c->h_stats[S_PRED2_TOTAL], p_max = c->h_stats[S_PRED2_MAX];
+            if (o.schedule_lpt == 3 || (double)p_max * (double)n_cur > 1.5 * (double)p_tot) {
+                uint32_t* lst = const_cast<uint32_t*>(cur);       // idsA or idsB (never ids0 here)
+                CK(sort_desc(key0, key1, lst, nxt, n_cur, p_max, cur));
+                nxt = (cur == idsA) ? idsB : idsA;
+                lpt = true;
+                st.lpt = 2;
+                break;
+            }
+        }
     }
 
     if (st.bulk_iters > 0) {

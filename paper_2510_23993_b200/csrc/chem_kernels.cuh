@@ -29,6 +29,7 @@ enum StatIdx {
     S_ATTEMPTED = 0, S_ACCEPTED, S_RHS, S_JAC, S_LU, S_NEWTON_FAIL, S_NONFINITE, S_TRANGE, S_UNFINISHED,
     S_DONE, S_DRIFT_BITS, S_COUNT_ACTIVE, S_CURSOR, S_FROZEN, S_WARP_SUBSTEPS, S_PRED_TOTAL, S_PRED_HEAVY,
     S_PRED_MAX,
+    S_PRED2_TOTAL, S_PRED2_MAX,   // in-call prediction after the first burst (sum, max of remaining substeps)
     S_SIG0, S_SIG1, S_SIG2,   // cell-layout signature of the workspace's cost hints (not cleared per call)
     S_HINT_MIN, S_HINT_MAX,   // sum over finished cells of min / max(hint, actual substeps): hint accuracy
     S_HINT_VALID,             // 1 if those sums describe valid hints (the call had the layout's history)
@@ -149,6 +150,31 @@ __global__ void __launch_bounds__(BS) k_gate(LaunchCtx L, uint32_t* ids_out, uin
             if ((threadIdx.x & 31) == 0 && mx) atomicMax(&L.stats[S_PRED_MAX], (unsigned long long)mx);
         }
         block_compact<BS>(act, (uint32_t)g, ids_out, &L.stats[S_COUNT_ACTIVE], prev, keys_out);
+    }
+}
+
+// In-call cost prediction (heavy-first without cross-call hints, chem_opts.schedule_lpt 2/3): after the
+// first bulk burst every still-active cell's remaining substeps are estimated from its own state as
+// (dt - t) / h (h = the step the controller proposes next); keys_out[i] pairs with ids[i].
+template <int BS>
+__global__ void __launch_bounds__(BS) k_predict(LaunchCtx L, const uint32_t* ids, int64_t n, uint32_t* keys_out)
+{
+    for (int64_t base = (int64_t)blockIdx.x * BS; base < n; base += (int64_t)gridDim.x * BS) {
+        const int64_t i = base + threadIdx.x;
+        uint32_t key = 0;
+        if (i < n) {
+            const uint32_t g = ids[i];
+            const double dt = L.boxes[L.cell_box[g]].dt;
+            const double h = L.cell_h[g];
+            const double rem = h > 0.0 ? (dt - L.cell_t[g]) / h : 16777215.0;
+            key = (uint32_t)fmin(fmax(rem, 1.0), 16777215.0);
+            keys_out[i] = key;
+        }
+        warp_add(&L.stats[S_PRED2_TOTAL], key);
+        unsigned mx = key;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if ((threadIdx.x & 31) == 0 && mx) atomicMax(&L.stats[S_PRED2_MAX], (unsigned long long)mx);
     }
 }
 

@@ -264,7 +264,7 @@ def test_virtual_ranks_bitwise(chem, ora, doc):
 @pytest.mark.parametrize("opts", [dict(kmax_bulk=20, n_active_star=3000),
                                   dict(compact_bulk=0, kmax_bulk=3), dict(lockstep=1),
                                   dict(lockstep=1, kmax_first=0, kmax_bulk=3), dict(lockstep=1, compact_bulk=0),
-                                  dict(schedule_lpt=1)])
+                                  dict(schedule_lpt=1), dict(schedule_lpt=3), dict(schedule_lpt=3, lockstep=1)])
 def test_cfg3_schedule_variants_bitwise(ora, doc, opts):
     """Bulk-sparse variants (longer bursts, the paper's all-cells bursts, lockstep, heavy-first) give
     bitwise the same field as the default schedule (P:177 / S:191), at full cfg3 size."""

@@ -479,11 +479,12 @@ def test_budget_equivalence_lpt_vs_alg3(ora):
     res = []
     for opts in (dict(schedule_lpt=0, kmax_bulk=5, n_active_star=0),
                  dict(schedule_lpt=0, kmax_bulk=3, n_active_star=64),
-                 dict(schedule_lpt=1), dict(schedule_lpt=0, n_active_star=10 ** 9)):
+                 dict(schedule_lpt=1), dict(schedule_lpt=0, n_active_star=10 ** 9),
+                 dict(schedule_lpt=3, kmax_bulk=2, n_active_star=0)):
         ch = Chem("h2air_li2004", device=0, kmax_sparse=12, **opts)
         _run_gpu(ch, rho, e, T0, Y, d["dt"])        # leaves cost hints (the heavy-first launch needs them)
         T, Yg, st = _run_gpu(ch, rho, e, T0, Y, d["dt"])
-        assert st["lpt"] == (1 if opts.get("schedule_lpt") == 1 else 0)
+        assert st["lpt"] == {1: 1, 3: 2}.get(opts.get("schedule_lpt"), 0), (opts, st["lpt"])
         res.append((T, Yg, ch.cell_status().cpu().numpy(), st["n_unfinished"], st["steps_attempted"]))
     assert res[0][3] > 0
     for r in res[1:]:
