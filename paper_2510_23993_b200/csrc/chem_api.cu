@@ -13,7 +13,6 @@
 #include "../../include/chem.h"
 #include "chem_launch.cuh"
 
-#include <cub/device/device_radix_sort.cuh>
 
 using namespace chem;
 
@@ -321,8 +320,6 @@ struct chem_ctx {
     int32_t* trace = nullptr;        // device [trace_rows][nboxes] activity trace (App. B), or null
     int32_t trace_rows = 0;
     double simt_eff = 1.0;           // bulk SIMT efficiency of the last call (lockstep = 2 input)
-    void* sort_tmp = nullptr;        // cub radix-sort scratch of the heavy-first schedule (library-owned)
-    size_t sort_tmp_bytes = 0;
     unsigned long long* h_sig = nullptr;   // pinned [6]: staging of the signature + hint-accuracy slots
     struct WsRecord { const void* ws; int64_t total; int32_t nboxes; };
     std::vector<WsRecord> ws_last;   // layout of the last call on each workspace (chem_cell_status)
@@ -447,7 +444,6 @@ void chem_finalize(chem_ctx* c)
     if (c->h_stats) cudaFreeHost(c->h_stats);
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
-    if (c->sort_tmp) cudaFree(c->sort_tmp);
     if (c->h_sig) cudaFreeHost(c->h_sig);
     delete c;
 }
@@ -700,8 +696,7 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
     CK(cudaMemcpyAsync(L.stats + S_SIG0, c->h_sig, 6 * sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
     const uint64_t pred_total = c->h_stats[S_PRED_TOTAL], pred_heavy = c->h_stats[S_PRED_HEAVY];
     const uint64_t pred_max = c->h_stats[S_PRED_MAX];
-    const bool sortable = n_active > 0 && n_active <= (int64_t)0x7fffffff;   // cub's int item count
-    const bool eligible = sortable && o.method != CHEM_METHOD_EXPLICIT;
+    const bool eligible = n_active > 0 && o.method != CHEM_METHOD_EXPLICIT;
     // hints that vary (max above 1.5x the mean) or put half the work in heavy cells
     const bool skewed = history && pred_total > 0 &&
                         (2 * pred_heavy >= pred_total ||
@@ -715,29 +710,23 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
     const uint32_t* cur = ids0;
     int64_t n_cur = n_active;
     uint32_t* nxt = idsA;
-    // stable descending radix sort of (keys, ids) over the bits in use; returns the sorted id list
-    auto sort_desc = [&](uint32_t* k_a, uint32_t* k_b, uint32_t* v_a, uint32_t* v_b, int64_t n, uint64_t kmax,
-                         const uint32_t*& out) -> cudaError_t {
-        cub::DoubleBuffer<uint32_t> dk(k_a, k_b), dv(v_a, v_b);
-        size_t need = 0;
-        int bits = 1;
-        while (bits < 32 && (1ull << bits) <= kmax) ++bits;
-        cudaError_t r = cub::DeviceRadixSort::SortPairsDescending(nullptr, need, dk, dv, (int)n, 0, bits, s);
+    // heavy-first order: counting sort of the list into cost buckets, heaviest first (k_bucket_*);
+    // the bucket histogram / cursors live in the workspace's key1 section
+    auto sort_desc = [&](const uint32_t* keys, const uint32_t* ids_in, int64_t n, uint32_t* ids_out) -> cudaError_t {
+        unsigned* hist = reinterpret_cast<unsigned*>(key1);
+        cudaError_t r = cudaMemsetAsync(hist, 0, sizeof(unsigned) * kCostBuckets, s);
         if (r != cudaSuccess) return r;
-        if (need > c->sort_tmp_bytes) {
-            if (c->sort_tmp) cudaFree(c->sort_tmp);
-            c->sort_tmp = nullptr;
-            c->sort_tmp_bytes = 0;
-            if ((r = cudaMalloc(&c->sort_tmp, need)) != cudaSuccess) return r;
-            c->sort_tmp_bytes = need;
-        }
-        r = cub::DeviceRadixSort::SortPairsDescending(c->sort_tmp, need, dk, dv, (int)n, 0, bits, s);
-        out = dv.Current();
-        return r;
+        const int g = grid_for(n, kStreamBS, c->num_sms * 8);
+        k_bucket_hist<kStreamBS><<<g, kStreamBS, 0, s>>>(keys, n, hist);
+        k_bucket_scan<<<1, 32, 0, s>>>(hist);
+        k_bucket_scatter<kStreamBS><<<g, kStreamBS, 0, s>>>(keys, ids_in, n, hist, ids_out);
+        return cudaGetLastError();
     };
     if (lpt) {
-        CK(sort_desc(key0, key1, ids0, idsA, n_active, pred_max, cur));
-        nxt = (cur == idsA) ? idsB : idsA;
+        // ids0 (the gate's list) stays intact for the box cost: the sorted list goes to idsA
+        CK(sort_desc(key0, ids0, n_active, idsA));
+        cur = idsA;
+        nxt = idsB;
     }
 
     // ---- Alg. 3 §2: bulk bursts while N_active > N*
@@ -796,8 +785,8 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
             CK(read_count(dummy));
             const uint64_t p_tot = c->h_stats[S_PRED2_TOTAL], p_max = c->h_stats[S_PRED2_MAX];
             if (o.schedule_lpt == 3 || (double)p_max * (double)n_cur > 1.5 * (double)p_tot) {
-                uint32_t* lst = const_cast<uint32_t*>(cur);       // idsA or idsB (never ids0 here)
-                CK(sort_desc(key0, key1, lst, nxt, n_cur, p_max, cur));
+                CK(sort_desc(key0, cur, n_cur, nxt));             // cur is idsA or idsB, never ids0
+                cur = nxt;
                 nxt = (cur == idsA) ? idsB : idsA;
                 lpt = true;
                 st.lpt = 2;

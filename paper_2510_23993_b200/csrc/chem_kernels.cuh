@@ -178,6 +178,55 @@ __global__ void __launch_bounds__(BS) k_predict(LaunchCtx L, const uint32_t* ids
     }
 }
 
+// Heavy-first ordering without a library sort: a counting sort of the cell list into 64 cost buckets
+// (bucket = floor(4 log2 cost): quarter-octave resolution up to 2^16 substeps), heaviest bucket first.
+// Order within a bucket follows the atomics (results never depend on the order, only the timing does).
+constexpr int kCostBuckets = 64;
+
+__device__ __forceinline__ int cost_bucket(uint32_t key)
+{
+    if (key <= 1u) return 0;
+    const int e = 31 - __clz(key);                         // floor(log2 key)
+    const int q = (int)((key >> (e >= 2 ? e - 2 : 0)) << (e >= 2 ? 0 : 2 - e)) & 3;   // next two bits
+    return min(kCostBuckets - 1, 4 * e + q);
+}
+
+template <int BS>
+__global__ void __launch_bounds__(BS) k_bucket_hist(const uint32_t* keys, int64_t n, unsigned* hist)
+{
+    __shared__ unsigned h[kCostBuckets];
+    for (int i = threadIdx.x; i < kCostBuckets; i += BS) h[i] = 0;
+    __syncthreads();
+    for (int64_t i = (int64_t)blockIdx.x * BS + threadIdx.x; i < n; i += (int64_t)gridDim.x * BS)
+        atomicAdd(&h[cost_bucket(keys[i])], 1u);
+    __syncthreads();
+    for (int i = threadIdx.x; i < kCostBuckets; i += BS)
+        if (h[i]) atomicAdd(&hist[i], h[i]);
+}
+
+// exclusive offsets, heaviest bucket first (one warp; hist -> cursor in place)
+static __global__ void k_bucket_scan(unsigned* hist)
+{
+    unsigned run = 0;
+    for (int b = kCostBuckets - 1; b >= 0; --b) {
+        if (threadIdx.x == 0) {
+            const unsigned c = hist[b];
+            hist[b] = run;
+            run += c;
+        }
+    }
+}
+
+template <int BS>
+__global__ void __launch_bounds__(BS) k_bucket_scatter(const uint32_t* keys, const uint32_t* ids_in, int64_t n,
+                                                       unsigned* cursor, uint32_t* ids_out)
+{
+    for (int64_t i = (int64_t)blockIdx.x * BS + threadIdx.x; i < n; i += (int64_t)gridDim.x * BS) {
+        const unsigned at = atomicAdd(&cursor[cost_bucket(keys[i])], 1u);
+        ids_out[at] = ids_in[i];
+    }
+}
+
 // ----------------------------------------------------------------------------- A8 compaction
 template <int BS>
 __global__ void __launch_bounds__(BS) k_compact(LaunchCtx L, const uint32_t* ids_in, int64_t n_in, uint32_t* ids_out)
