@@ -710,16 +710,14 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
     const uint32_t* cur = ids0;
     int64_t n_cur = n_active;
     uint32_t* nxt = idsA;
-    // heavy-first order: counting sort of the list into cost buckets, heaviest first (k_bucket_*);
-    // the bucket histogram / cursors live in the workspace's key1 section
+    // heavy-first order: stable counting sort of the list into cost buckets, heaviest first
+    // (k_bucket_*); the per-tile histogram lives in the workspace's key1 section (n/16 entries)
     auto sort_desc = [&](const uint32_t* keys, const uint32_t* ids_in, int64_t n, uint32_t* ids_out) -> cudaError_t {
         unsigned* hist = reinterpret_cast<unsigned*>(key1);
-        cudaError_t r = cudaMemsetAsync(hist, 0, sizeof(unsigned) * kCostBuckets, s);
-        if (r != cudaSuccess) return r;
-        const int g = grid_for(n, kStreamBS, c->num_sms * 8);
-        k_bucket_hist<kStreamBS><<<g, kStreamBS, 0, s>>>(keys, n, hist);
-        k_bucket_scan<<<1, 32, 0, s>>>(hist);
-        k_bucket_scatter<kStreamBS><<<g, kStreamBS, 0, s>>>(keys, ids_in, n, hist, ids_out);
+        const int ntiles = (int)((n + kSortTile - 1) / kSortTile);
+        k_bucket_hist<<<ntiles, kSortBS, 0, s>>>(keys, n, hist, ntiles);
+        k_scan_excl<<<1, 1024, 0, s>>>(hist, (int64_t)ntiles * kCostBuckets);
+        k_bucket_scatter<<<ntiles, kSortBS, 0, s>>>(keys, ids_in, n, hist, ntiles, ids_out);
         return cudaGetLastError();
     };
     if (lpt) {

@@ -178,52 +178,100 @@ __global__ void __launch_bounds__(BS) k_predict(LaunchCtx L, const uint32_t* ids
     }
 }
 
-// Heavy-first ordering without a library sort: a counting sort of the cell list into 64 cost buckets
-// (bucket = floor(4 log2 cost): quarter-octave resolution up to 2^16 substeps), heaviest bucket first.
-// Order within a bucket follows the atomics (results never depend on the order, only the timing does).
+// Heavy-first ordering without a library sort: a STABLE counting sort of the cell list into 64 cost
+// buckets (bucket = floor(4 log2 cost): quarter-octave resolution up to 2^16 substeps), heaviest bucket
+// first; within a bucket the list order is kept (neighbouring cells stay together: coalesced loads and
+// similar cells per warp).  Three passes over tiles of kSortTile entries:
+//   k_bucket_hist    per-tile bucket counts -> hist[(63 - bucket) * ntiles + tile]
+//   k_scan_excl      exclusive scan of hist (heaviest bucket first, tiles in order)
+//   k_bucket_scatter each tile places its entries in order (warp match + per-warp prefix)
 constexpr int kCostBuckets = 64;
+constexpr int kSortBS = 256;
+constexpr int kSortTile = 4 * kSortBS;
 
 __device__ __forceinline__ int cost_bucket(uint32_t key)
 {
     if (key <= 1u) return 0;
     const int e = 31 - __clz(key);                         // floor(log2 key)
-    const int q = (int)((key >> (e >= 2 ? e - 2 : 0)) << (e >= 2 ? 0 : 2 - e)) & 3;   // next two bits
+    const int q = e >= 2 ? (int)(key >> (e - 2)) & 3 : (int)(key << (2 - e)) & 3;   // next two bits
     return min(kCostBuckets - 1, 4 * e + q);
 }
 
-template <int BS>
-__global__ void __launch_bounds__(BS) k_bucket_hist(const uint32_t* keys, int64_t n, unsigned* hist)
+static __global__ void __launch_bounds__(kSortBS) k_bucket_hist(const uint32_t* keys, int64_t n, unsigned* hist,
+                                                         int ntiles)
 {
     __shared__ unsigned h[kCostBuckets];
-    for (int i = threadIdx.x; i < kCostBuckets; i += BS) h[i] = 0;
+    for (int i = threadIdx.x; i < kCostBuckets; i += kSortBS) h[i] = 0;
     __syncthreads();
-    for (int64_t i = (int64_t)blockIdx.x * BS + threadIdx.x; i < n; i += (int64_t)gridDim.x * BS)
-        atomicAdd(&h[cost_bucket(keys[i])], 1u);
+    const int64_t base = (int64_t)blockIdx.x * kSortTile;
+    for (int r = 0; r < kSortTile / kSortBS; ++r) {
+        const int64_t i = base + r * kSortBS + threadIdx.x;
+        if (i < n) atomicAdd(&h[cost_bucket(keys[i])], 1u);
+    }
     __syncthreads();
-    for (int i = threadIdx.x; i < kCostBuckets; i += BS)
-        if (h[i]) atomicAdd(&hist[i], h[i]);
+    for (int b = threadIdx.x; b < kCostBuckets; b += kSortBS) hist[(kCostBuckets - 1 - b) * ntiles + blockIdx.x] = h[b];
 }
 
-// exclusive offsets, heaviest bucket first (one warp; hist -> cursor in place)
-static __global__ void k_bucket_scan(unsigned* hist)
+// exclusive scan of m entries in place, one block of 1024 threads
+static __global__ void __launch_bounds__(1024) k_scan_excl(unsigned* v, int64_t m)
 {
-    unsigned run = 0;
-    for (int b = kCostBuckets - 1; b >= 0; --b) {
-        if (threadIdx.x == 0) {
-            const unsigned c = hist[b];
-            hist[b] = run;
-            run += c;
-        }
+    __shared__ unsigned part[1024];
+    const int64_t per = (m + 1023) / 1024;
+    const int64_t lo = threadIdx.x * per, hi = min(m, lo + per);
+    unsigned s = 0;
+    for (int64_t i = lo; i < hi; ++i) s += v[i];
+    part[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {               // Hillis-Steele inclusive scan of the partials
+        const unsigned add = threadIdx.x >= o ? part[threadIdx.x - o] : 0u;
+        __syncthreads();
+        part[threadIdx.x] += add;
+        __syncthreads();
+    }
+    unsigned run = threadIdx.x ? part[threadIdx.x - 1] : 0u;
+    for (int64_t i = lo; i < hi; ++i) {
+        const unsigned c = v[i];
+        v[i] = run;
+        run += c;
     }
 }
 
-template <int BS>
-__global__ void __launch_bounds__(BS) k_bucket_scatter(const uint32_t* keys, const uint32_t* ids_in, int64_t n,
-                                                       unsigned* cursor, uint32_t* ids_out)
+static __global__ void __launch_bounds__(kSortBS) k_bucket_scatter(const uint32_t* keys, const uint32_t* ids_in, int64_t n,
+                                                            const unsigned* offs, int ntiles, uint32_t* ids_out)
 {
-    for (int64_t i = (int64_t)blockIdx.x * BS + threadIdx.x; i < n; i += (int64_t)gridDim.x * BS) {
-        const unsigned at = atomicAdd(&cursor[cost_bucket(keys[i])], 1u);
-        ids_out[at] = ids_in[i];
+    constexpr int NW = kSortBS / 32;
+    __shared__ unsigned run[kCostBuckets];             // entries of each bucket placed by earlier rounds
+    __shared__ unsigned tot[kCostBuckets];             // this round's entries per bucket
+    __shared__ unsigned wcnt[NW][kCostBuckets];        // this round: per-warp counts -> exclusive prefixes
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int b = threadIdx.x; b < kCostBuckets; b += kSortBS) run[b] = 0;
+    const int64_t base = (int64_t)blockIdx.x * kSortTile;
+    for (int r = 0; r < kSortTile / kSortBS; ++r) {
+        for (int b = threadIdx.x; b < NW * kCostBuckets; b += kSortBS) (&wcnt[0][0])[b] = 0;
+        __syncthreads();
+        const int64_t i = base + r * kSortBS + threadIdx.x;
+        const bool valid = i < n;
+        const int bk = valid ? cost_bucket(keys[i]) : kCostBuckets;    // invalid lanes: a bucket of their own
+        const unsigned peers = __match_any_sync(0xffffffffu, bk);
+        const unsigned rank = __popc(peers & ((1u << lane) - 1u));
+        if (valid && rank == 0) wcnt[w][bk] = __popc(peers);
+        __syncthreads();
+        if (threadIdx.x < kCostBuckets) {               // per bucket: exclusive prefix over the warps
+            unsigned acc = 0;
+            for (int ww = 0; ww < NW; ++ww) {
+                const unsigned c = wcnt[ww][threadIdx.x];
+                wcnt[ww][threadIdx.x] = acc;
+                acc += c;
+            }
+            tot[threadIdx.x] = acc;
+        }
+        __syncthreads();
+        if (valid) {
+            const unsigned at = offs[(kCostBuckets - 1 - bk) * ntiles + blockIdx.x] + run[bk] + wcnt[w][bk] + rank;
+            ids_out[at] = ids_in[i];
+        }
+        __syncthreads();
+        if (threadIdx.x < kCostBuckets) run[threadIdx.x] += tot[threadIdx.x];
     }
 }
 
