@@ -711,7 +711,7 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
     int64_t n_cur = n_active;
     uint32_t* nxt = idsA;
     // heavy-first order: stable counting sort of the list into cost buckets, heaviest first
-    // (k_bucket_*); the per-tile histogram lives in the workspace's key1 section (n/16 entries)
+    // (k_bucket_*); the per-tile histogram lives in the workspace's key1 section (n/4 entries)
     auto sort_desc = [&](const uint32_t* keys, const uint32_t* ids_in, int64_t n, uint32_t* ids_out) -> cudaError_t {
         unsigned* hist = reinterpret_cast<unsigned*>(key1);
         const int ntiles = (int)((n + kSortTile - 1) / kSortTile);

@@ -178,23 +178,24 @@ __global__ void __launch_bounds__(BS) k_predict(LaunchCtx L, const uint32_t* ids
     }
 }
 
-// Heavy-first ordering without a library sort: a STABLE counting sort of the cell list into 64 cost
-// buckets (bucket = floor(4 log2 cost): quarter-octave resolution up to 2^16 substeps), heaviest bucket
+// Heavy-first ordering without a library sort: a STABLE counting sort of the cell list into 256 cost
+// buckets (bucket = floor(16 log2 cost): 1/16-octave resolution up to 2^16 substeps), heaviest bucket
 // first; within a bucket the list order is kept (neighbouring cells stay together: coalesced loads and
 // similar cells per warp).  Three passes over tiles of kSortTile entries:
-//   k_bucket_hist    per-tile bucket counts -> hist[(63 - bucket) * ntiles + tile]
+//   k_bucket_hist    per-tile bucket counts -> hist[(255 - bucket) * ntiles + tile]
 //   k_scan_excl      exclusive scan of hist (heaviest bucket first, tiles in order)
 //   k_bucket_scatter each tile places its entries in order (warp match + per-warp prefix)
-constexpr int kCostBuckets = 64;
+constexpr int kCostBuckets = 256;
 constexpr int kSortBS = 256;
 constexpr int kSortTile = 4 * kSortBS;
 
+// bucket = floor(16 log2 key) (1/16-octave resolution up to 2^16 substeps): 4 bits below the leading one
 __device__ __forceinline__ int cost_bucket(uint32_t key)
 {
     if (key <= 1u) return 0;
     const int e = 31 - __clz(key);                         // floor(log2 key)
-    const int q = e >= 2 ? (int)(key >> (e - 2)) & 3 : (int)(key << (2 - e)) & 3;   // next two bits
-    return min(kCostBuckets - 1, 4 * e + q);
+    const int q = e >= 4 ? (int)(key >> (e - 4)) & 15 : (int)(key << (4 - e)) & 15;
+    return min(kCostBuckets - 1, 16 * e + q);
 }
 
 static __global__ void __launch_bounds__(kSortBS) k_bucket_hist(const uint32_t* keys, int64_t n, unsigned* hist,
