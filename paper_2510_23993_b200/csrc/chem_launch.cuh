@@ -10,6 +10,11 @@
 namespace chem {
 
 constexpr int kIntegrateBS = 32;   // threads per block of the free-running k_integrate
+#ifdef CHEM_SMEM_PAD
+constexpr size_t kSmemPad = CHEM_SMEM_PAD;
+#else
+constexpr size_t kSmemPad = 0;
+#endif
 
 template <class M, class Meth>
 struct Launch {
@@ -20,7 +25,8 @@ struct Launch {
     static cudaError_t lock(const Params<M>& p, const LaunchCtx& L, const uint32_t* ids, int64_t n, int kmax,
                             int refill, int fin, int nsm, cudaStream_t s);
     static int blocks_per_sm();
-    static constexpr size_t smem() { return (size_t)SmemLayout<M, Meth>::bytes_per_thread * kIntegrateBS; }
+    // CHEM_SMEM_PAD (experiment builds only): extra bytes per block, to lower the resident blocks per SM
+    static constexpr size_t smem() { return (size_t)SmemLayout<M, Meth>::bytes_per_thread * kIntegrateBS + kSmemPad; }
 };
 
 }  // namespace chem
