@@ -655,7 +655,12 @@ def ours(args):
             return [dict(rho=b.rho.cpu().pin_memory(), e=b.e.cpu().pin_memory(), T=b.T.cpu().pin_memory(),
                          Y=b.Y.cpu().pin_memory(), dt=b.dt) for b in wl.boxes]
         sets = [host_set(1000)] + ([host_set(1001)] if wl.evolve != "restore" else [])
-        chunks = args.e2e_chunks if args.e2e_chunks > 0 else (5 if args.config in ("cfg2", "cfg5") else 1)
+        # copy/compute pipelining groups: dense fields split into ~0.5 GB groups (3..12; measured r02:
+        # cfg2 3 groups 147 vs 5 groups 144, cfg5 12 groups 181 vs 5 groups 167 Mcell-steps/s); the
+        # detonation fields run as one call (splitting them splits the heavy-first schedule)
+        field_bytes = sum(b.ncells * (3 + b.Y.shape[0]) * 8 for b in wl.boxes)
+        chunks = args.e2e_chunks if args.e2e_chunks > 0 else \
+            (int(min(12, max(3, round(field_bytes / 0.5e9)))) if args.config in ("cfg2", "cfg5") else 1)
         hr = HostRunner(chem, sets[0], wl.calls, chunks=chunks)
         for k in range(2):
             hr.load_inputs(sets[k % len(sets)])
