@@ -19,9 +19,9 @@ Inputs between timed steps (untimed, before the start event) — VERDICT r01 nex
     +-1 % T jitter with e recomputed, which knocks burnt cells off equilibrium and so inflates
     the work; kept as an option.)  The line also reports the first call of a layout (no cost
     hints), Alg. 3 as written (schedule_lpt = 0) and exact replay (restore), timed the same way.
-With no flags (the driver's command) the cfg2 headline line carries, under "also", the cfg3
-bulk-sparse field timed under Alg. 3 and under the default schedule, so the driver measures a
-non-empty sparse phase.
+With no flags (the driver's command) the cfg2 headline line carries, under "also", the cfg2b variant
+(t/tau ~ U[0.85, 0.95] per cell) and the cfg3 bulk-sparse field timed under Alg. 3 and under the
+default schedule, so the driver measures intra-warp divergence and a non-empty sparse phase.
 
 Multi-GPU: cells are independent 0-D reactors, so every rank integrates its own
 boxes with no data-path collective.  NCCL carries the cost all_gather of the LPT balance (cfg4,
@@ -68,7 +68,7 @@ def parse():
                    help="inputs between steps (auto: restore for cfg2, shift otherwise)")
     p.add_argument("--perturb", type=float, default=0.01, help="relative T jitter of --evolve perturb")
     p.add_argument("--also", default="auto",
-                   help="extra configs timed into the same line ('auto': cfg3 when --config cfg2; 'none')")
+                   help="extra configs timed into the same line ('auto': cfg2b and cfg3 when --config cfg2; 'none')")
     p.add_argument("--no-schedules", action="store_true", help="skip the first-call / alg3 / replay variants")
     p.add_argument("--no-prod", action="store_true", help="skip the production-tolerance number")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -276,6 +276,10 @@ def build_workload(args, chem, doc, device, rank, world, config=None, evolve="au
                                                              args.perturb, extra)
     if config == "cfg2":
         raw, meta = synth.field_cfg2(doc, device=device)
+        boxes = _mk_boxes(chem, raw)
+        return mk(boxes, [list(range(len(boxes)))], meta, sum(b.ncells for b in boxes))
+    if config == "cfg2b":
+        raw, meta = synth.field_cfg2b(doc, device=device)
         boxes = _mk_boxes(chem, raw)
         return mk(boxes, [list(range(len(boxes)))], meta, sum(b.ncells for b in boxes))
     if config == "cfg3":
@@ -660,7 +664,7 @@ def ours(args):
         # detonation fields run as one call (splitting them splits the heavy-first schedule)
         field_bytes = sum(b.ncells * (3 + b.Y.shape[0]) * 8 for b in wl.boxes)
         chunks = args.e2e_chunks if args.e2e_chunks > 0 else \
-            (int(min(12, max(3, round(field_bytes / 0.5e9)))) if args.config in ("cfg2", "cfg5") else 1)
+            (int(min(12, max(3, round(field_bytes / 0.5e9)))) if args.config in ("cfg2", "cfg2b", "cfg5") else 1)
         hr = HostRunner(chem, sets[0], wl.calls, chunks=chunks)
         for k in range(2):
             hr.load_inputs(sets[k % len(sets)])
@@ -704,7 +708,7 @@ def ours(args):
 
     # extra configs timed into the same line (the driver runs only the default command)
     also = []
-    also_cfgs = (["cfg3"] if args.config == "cfg2" else []) if args.also == "auto" else \
+    also_cfgs = (["cfg2b", "cfg3"] if args.config == "cfg2" else []) if args.also == "auto" else \
         [c for c in args.also.split(",") if c and c != "none"]
     if world == 1 and also_cfgs:
         meta_main, wl_cells, wl_cs, wl_calls, wl_extra = wl.meta, ncells, wl.cell_steps, len(wl.calls), wl.extra

@@ -141,6 +141,26 @@ def field_cfg2(doc, side=128, box=32, device="cuda", dt=1e-7):
     return boxes, meta
 
 
+def field_cfg2b(doc, side=128, box=32, device="cuda", dt=1e-7, seed=SEED0 + 12):
+    """configs[1] variant 2b: the cfg2 field with every cell's trajectory time drawn
+    per cell, t/tau ~ U[0.85, 0.95] (counter-based hash of the global cell index), so neighbouring
+    cells need different substep counts (intra-warp divergence on an otherwise uniform field)."""
+    import torch
+    tab = _traj_tables(doc, "fresh", device, T0=1200.0)
+    nb1 = side // box
+    n = box ** 3
+    boxes = []
+    for b in range(nb1 ** 3):
+        gidx = torch.arange(b * n, (b + 1) * n, device=device, dtype=torch.int64)
+        frac = 0.85 + 0.1 * hash_uniform(gidx, seed)
+        T, Y = _lookup(tab, frac)
+        boxes.append(dict(rho=torch.full((n,), tab["rho"], dtype=torch.float64, device=device), T=T.clone(),
+                          Y=Y.T.contiguous(), dt=dt))
+    meta = dict(workload=f"cfg2b: {side}^3 H2-air field, T0=1200 K traj. states at t/tau ~ U[0.85, 0.95] per cell, "
+                         f"{nb1 ** 3} boxes of {box}^3, dt={dt:g} s", cells=side ** 3)
+    return boxes, meta
+
+
 # ------------------------------------------------------------------ counter-based randomness
 def hash_uniform(idx, seed):
     """Uniform [0, 1) from a 32-bit integer hash of (idx, seed); idx is an int64 torch tensor.

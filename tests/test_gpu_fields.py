@@ -160,6 +160,21 @@ def test_cfg2_full_size(chem, ora, doc):
     assert np.allclose(c, c[0]) and np.isclose(c.sum(), st["steps_attempted"])
 
 
+def test_cfg2b_full_size(chem, ora, doc):
+    """cfg2 variant 2b (t/tau ~ U[0.85, 0.95] per cell): the full 128^3 field against the oracle on 64
+    random cells plus the 1000 that took the most substeps."""
+    raw, meta = synth.field_cfg2b(doc, device=DEV)
+    fr = torch.cat([r["T"] for r in raw])
+    assert len(torch.unique(fr)) >= 5                  # several states mixed cell by cell
+    boxes, st, cost = _run(chem, raw)
+    assert st["cells"] == 128 ** 3 and st["n_unfinished"] == 0 and st["n_nonfinite"] == 0
+    rng = np.random.default_rng(6)
+    picks = [(int(rng.integers(0, 64)), int(rng.integers(0, 32 ** 3))) for _ in range(64)]
+    hard, steps = _hardest(chem, raw)
+    assert steps.max() > steps[steps > 0].min()        # cells differ in cost (intra-warp divergence)
+    _sample_and_check(ora, raw, boxes, picks + hard, converge=True)
+
+
 def test_cfg3_full_size(ora, doc):
     """cfg3 at 256^3 in the bench's launch configuration: the first (hint-less, Alg. 3) call and the
     second (heavy-first) call are bitwise equal; the second is compared with the oracle on 4 random
