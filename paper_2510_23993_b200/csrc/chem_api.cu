@@ -736,8 +736,8 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
     // N* (P:181): negative = one resident wave of the integration kernel (SMs x resident cells per SM):
     // below it a bulk burst can no longer fill the GPU, so the persistent sparse launch takes over
     // (B200 sweep, profiles/r01_nstar_sweep.txt; the paper's 1e4 was tuned on H100).
-    const int64_t nstar = o.n_active_star >= 0 ? o.n_active_star
-                                               : (int64_t)c->num_sms * ops.blocks_per_sm(o.method) * kIntegrateBS;
+    const int64_t wave = (int64_t)c->num_sms * ops.blocks_per_sm(o.method) * kIntegrateBS;   // resident cells
+    const int64_t nstar = o.n_active_star >= 0 ? o.n_active_star : wave;
     while (!lpt && n_cur > nstar && n_cur > 0) {
         const bool first_burst = lock && st.bulk_iters == 0 && o.kmax_first > 0;
         const int kmax_b = first_burst ? o.kmax_first : o.kmax_bulk;
@@ -773,7 +773,8 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
         }
         cur = nxt;
         nxt = (nxt == idsA) ? idsB : idsA;
-        if (predict && st.bulk_iters == 1 && n_cur > nstar) {
+        // (the order matters only while more cells remain than one resident wave holds)
+        if (predict && st.bulk_iters == 1 && n_cur > wave) {
             // heavy-first on in-call predictions: the remaining substeps (dt - t)/h of every cell still
             // active after the first burst; skewed (max > 1.5 mean) or forced -> sort, one persistent launch
             CK(cudaMemsetAsync(L.stats + S_PRED2_TOTAL, 0, 16, s));
