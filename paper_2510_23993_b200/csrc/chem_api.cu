@@ -774,7 +774,7 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
         cur = nxt;
         nxt = (nxt == idsA) ? idsB : idsA;
         // (the order matters only while more cells remain than one resident wave holds)
-        if (predict && st.bulk_iters == 1 && n_cur > wave) {
+        if (predict && st.bulk_iters == 1 && n_cur > 0 && (o.schedule_lpt == 3 || n_cur > wave)) {
             // heavy-first on in-call predictions: the remaining substeps (dt - t)/h of every cell still
             // active after the first burst; skewed (max > 1.5 mean) or forced -> sort, one persistent launch
             CK(cudaMemsetAsync(L.stats + S_PRED2_TOTAL, 0, 16, s));
