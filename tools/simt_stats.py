@@ -21,15 +21,16 @@ def main():
     dev = torch.device("cuda", 0)
     for cfg in cfgs:
         chem = Chem("h2air_li2004", device=0, atol_T=bench.ATOL_T)
-        a = argparse.Namespace(config=cfg, rtol=bench.RTOL, atol=bench.ATOL, balance="none")
-        wl = bench.build_workload(a, chem, doc, dev, 0, 1)
+        a = argparse.Namespace(config=cfg, rtol=bench.RTOL, atol=bench.ATOL, balance="none", perturb=0.01,
+                               evolve="auto")
+        wl = bench.build_workload(a, chem, doc, dev, 0, 1, config=cfg)
         for lock in (0, 1, 2, 2):
             chem.set_opts(lockstep=lock)
-            wl.restore()
+            wl.prepare(0)
             torch.cuda.synchronize()
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s.record()
-            st = wl.step(chem, bench.RTOL, bench.ATOL)
+            st = wl.step(bench.RTOL, bench.ATOL)
             e.record()
             torch.cuda.synchronize()
             ws = sum(x["warp_substeps"] for x in st)
