@@ -287,7 +287,11 @@ class Chem:
 
 class HostRunner:
     """End-to-end public-API path for host-resident data (the bench's `e2e` leg): pinned host
-    buffers -> H2D copies -> chem_integrate_boxes -> D2H of (T, Y).
+    buffers -> H2D copies -> chem_integrate_boxes -> D2H of (T, Y), in place on the host like the
+    device API: each group's pinned slab [rho_*][e_*][T_*][Y_*] is copied to the device in one H2D
+    copy and its [T_*][Y_*] results come back into the same slab.  Only boxes the step touched
+    (box_cost > 0: at least one active cell) are copied back; an untouched box's host T, Y are already
+    its outputs (gated cells are bitwise untouched).
 
     With a single fused call per step, the boxes are processed in `chunks` groups through three
     CUDA streams so that the H2D copy of group i+1 and the D2H copy of group i-1 run on the copy
@@ -311,71 +315,96 @@ class HostRunner:
             self.s_d2h = torch.cuda.Stream(dev)
         else:
             self.groups = [list(range(nb))]
-        # One pinned input slab, one pinned output slab and one device slab per group, laid out as
-        # [rho_*][e_*][T_*][Y_*] (component-major boxes back to back): a step moves each group with ONE
-        # H2D copy of the slab and ONE D2H copy of its [T_*][Y_*] tail, instead of 4 + 2 copies per box.
         self.dev_boxes = [None] * nb
         self.out_T, self.out_Y = [None] * nb, [None] * nb
+        self.ranges = [None] * nb          # per box: (group, T offset, n, Y offset, ns * n) in the slab
         self.slabs = []
-        for grp in self.groups:
+        for g, grp in enumerate(self.groups):
             n = [host_boxes[i]["rho"].numel() for i in grp]
             ns = [host_boxes[i]["Y"].shape[0] for i in grp]
             tot = sum(n)
             size = 3 * tot + sum(a * c for a, c in zip(n, ns))
-            h_in = torch.empty(size, dtype=torch.float64).pin_memory()
-            h_out = torch.empty(size - 2 * tot, dtype=torch.float64).pin_memory()
+            h = torch.empty(size, dtype=torch.float64).pin_memory()
             d = torch.empty(size, dtype=torch.float64, device=dev)
             o = [0, tot, 2 * tot, 3 * tot]   # rho, e, T, Y cursors
             for i, ni, si in zip(grp, n, ns):
-                h = host_boxes[i]
-                h_in[o[0]:o[0] + ni].copy_(h["rho"].reshape(-1))
-                h_in[o[1]:o[1] + ni].copy_(h["e"].reshape(-1))
-                h_in[o[2]:o[2] + ni].copy_(h["T"].reshape(-1))
-                h_in[o[3]:o[3] + ni * si].copy_(h["Y"].reshape(-1))
                 self.dev_boxes[i] = Box(d[o[0]:o[0] + ni], d[o[1]:o[1] + ni], d[o[2]:o[2] + ni],
-                                        d[o[3]:o[3] + ni * si].view(si, ni), h["dt"])
-                self.out_T[i] = h_out[o[2] - 2 * tot:o[2] - 2 * tot + ni]
-                self.out_Y[i] = h_out[o[3] - 2 * tot:o[3] - 2 * tot + ni * si].view(si, ni)
+                                        d[o[3]:o[3] + ni * si].view(si, ni), host_boxes[i]["dt"])
+                self.out_T[i] = h[o[2]:o[2] + ni]
+                self.out_Y[i] = h[o[3]:o[3] + ni * si].view(si, ni)
+                self.ranges[i] = (g, o[2], ni, o[3], ni * si)
                 o = [o[0] + ni, o[1] + ni, o[2] + ni, o[3] + ni * si]
-            self.slabs.append((h_in, h_out, d, 2 * tot))
+            self.slabs.append((h, d, 2 * tot))
+        self.load_inputs(host_boxes)
         self.h2d_bytes = sum(s_[0].numel() * 8 for s_ in self.slabs)
-        self.d2h_bytes = sum(s_[1].numel() * 8 for s_ in self.slabs)
+        self.d2h_bytes_full = sum((s_[0].numel() - s_[2]) * 8 for s_ in self.slabs)
+        self.d2h_bytes = 0                  # of the last step (touched boxes only)
 
     def load_inputs(self, host_boxes):
-        """Copy new host inputs (same shapes as at construction) into the pinned input slabs (host
-        memcpy; the next step() moves them)."""
+        """Copy new host inputs (same shapes as at construction) into the pinned slabs (host memcpy;
+        the next step() moves them).  Needed before every step whose inputs are not the previous
+        step's outputs (the slabs are updated in place)."""
+        torch.cuda.synchronize(self.chem.device)    # the last step's D2H writes these slabs
         for g, grp in enumerate(self.groups):
-            h_in = self.slabs[g][0]
+            h = self.slabs[g][0]
             tot = sum(host_boxes[i]["rho"].numel() for i in grp)
             o = [0, tot, 2 * tot, 3 * tot]
             for i in grp:
-                h = host_boxes[i]
-                ni, si = h["rho"].numel(), h["Y"].shape[0]
-                h_in[o[0]:o[0] + ni].copy_(h["rho"].reshape(-1))
-                h_in[o[1]:o[1] + ni].copy_(h["e"].reshape(-1))
-                h_in[o[2]:o[2] + ni].copy_(h["T"].reshape(-1))
-                h_in[o[3]:o[3] + ni * si].copy_(h["Y"].reshape(-1))
+                hb = host_boxes[i]
+                ni, si = hb["rho"].numel(), hb["Y"].shape[0]
+                h[o[0]:o[0] + ni].copy_(hb["rho"].reshape(-1))
+                h[o[1]:o[1] + ni].copy_(hb["e"].reshape(-1))
+                h[o[2]:o[2] + ni].copy_(hb["T"].reshape(-1))
+                h[o[3]:o[3] + ni * si].copy_(hb["Y"].reshape(-1))
                 o = [o[0] + ni, o[1] + ni, o[2] + ni, o[3] + ni * si]
 
     def _h2d_group(self, g):
-        h_in, _, d, _ = self.slabs[g]
-        d.copy_(h_in, non_blocking=True)
+        h, d, _ = self.slabs[g]
+        d.copy_(h, non_blocking=True)
 
-    def _d2h_group(self, g):
-        _, h_out, d, t0 = self.slabs[g]
-        h_out.copy_(d[t0:], non_blocking=True)
+    def _d2h_boxes(self, boxes):
+        """D2H of the [T][Y] results of `boxes` into their slabs: one copy per group when every box
+        of the group is touched, else two per touched box."""
+        by_group = {}
+        for i in boxes:
+            by_group.setdefault(self.ranges[i][0], []).append(i)
+        nbytes = 0
+        for g, ids in by_group.items():
+            h, d, t0 = self.slabs[g]
+            if len(ids) == len(self.groups[g]):
+                h[t0:].copy_(d[t0:], non_blocking=True)
+                nbytes += (h.numel() - t0) * 8
+                continue
+            for i in ids:
+                _, to, n, yo, ny = self.ranges[i]
+                h[to:to + n].copy_(d[to:to + n], non_blocking=True)
+                h[yo:yo + ny].copy_(d[yo:yo + ny], non_blocking=True)
+                nbytes += (n + ny) * 8
+        return nbytes
+
+    def _call(self, ids, rtol, atol):
+        cost = torch.zeros(len(ids), dtype=torch.float64, device=self.chem.device)
+        st = self.chem.integrate_boxes([self.dev_boxes[i] for i in ids], rtol=rtol, atol=atol, box_cost=cost)
+        touched = [i for i, c in zip(ids, cost.cpu().tolist()) if c > 0]   # the call has synchronised
+        return st, touched
 
     def step(self, rtol, atol):
         if not self.pipelined:
             self._h2d_group(0)
-            st = [self.chem.integrate_boxes([self.dev_boxes[i] for i in c], rtol=rtol, atol=atol) for c in self.calls]
-            self._d2h_group(0)
+            st, touched = [], set()
+            for c in self.calls:
+                s_, t_ = self._call(c, rtol, atol)
+                st.append(s_)
+                touched.update(t_)
+            self.d2h_bytes = self._d2h_boxes(sorted(touched))
             return st
         comp = torch.cuda.current_stream(self.chem.device)
         ev_in = [torch.cuda.Event() for _ in self.groups]
         st = []
+        nbytes = 0
         with torch.cuda.stream(self.s_h2d):
             self.s_h2d.wait_stream(comp)            # the previous step's D2H reads must not be overwritten early
+            self.s_h2d.wait_stream(self.s_d2h)
             self._h2d_group(0)
             ev_in[0].record(self.s_h2d)
         for g, idx in enumerate(self.groups):
@@ -384,13 +413,15 @@ class HostRunner:
                     self._h2d_group(g + 1)
                     ev_in[g + 1].record(self.s_h2d)
             comp.wait_event(ev_in[g])
-            st.append(self.chem.integrate_boxes([self.dev_boxes[i] for i in idx], rtol=rtol, atol=atol))
+            s_, touched = self._call(idx, rtol, atol)
+            st.append(s_)
             done = torch.cuda.Event()
             done.record(comp)
             with torch.cuda.stream(self.s_d2h):
                 self.s_d2h.wait_event(done)
-                self._d2h_group(g)
+                nbytes += self._d2h_boxes(touched)
         comp.wait_stream(self.s_d2h)                # the step ends when the last result is on the host
+        self.d2h_bytes = nbytes
         return st
 
 

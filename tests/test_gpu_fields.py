@@ -334,12 +334,23 @@ def test_host_runner_matches_device_path(chem, doc, chunks):
     hr = HostRunner(chem, host, chunks=chunks)
     assert hr.pipelined == (chunks > 1)
     for _ in range(2):                                   # a second step starts from the same inputs
+        hr.load_inputs(host)
         hr.step(**GPU_TOL)
         torch.cuda.synchronize()
         for i, b in enumerate(dev_boxes):
             assert torch.equal(hr.out_T[i], b.T.cpu()) and torch.equal(hr.out_Y[i], b.Y.cpu())
     assert hr.h2d_bytes == 6 * 512 * (3 + len(doc["species"])) * 8
-    assert hr.d2h_bytes == 6 * 512 * (1 + len(doc["species"])) * 8
+    assert hr.d2h_bytes == 6 * 512 * (1 + len(doc["species"])) * 8       # every box active
+    # an all-cold box is not copied back: its host data are its outputs already
+    cold = dict(host[0])
+    cold["T"] = torch.full_like(host[0]["T"], 300.0).pin_memory()
+    cold["e"] = chem.energy(cold["T"].to(DEV), host[0]["Y"].to(DEV)).cpu().pin_memory()
+    host2 = [cold] + host[1:]
+    hr.load_inputs(host2)
+    hr.step(**GPU_TOL)
+    torch.cuda.synchronize()
+    assert hr.d2h_bytes == 5 * 512 * (1 + len(doc["species"])) * 8
+    assert torch.equal(hr.out_T[0], cold["T"]) and torch.equal(hr.out_Y[0], cold["Y"])
     del rng
 
 
