@@ -659,12 +659,12 @@ def ours(args):
             return [dict(rho=b.rho.cpu().pin_memory(), e=b.e.cpu().pin_memory(), T=b.T.cpu().pin_memory(),
                          Y=b.Y.cpu().pin_memory(), dt=b.dt) for b in wl.boxes]
         sets = [host_set(1000)] + ([host_set(1001)] if wl.evolve != "restore" else [])
-        # copy/compute pipelining groups: dense fields split into ~0.5 GB groups (3..12; measured r02:
+        # copy/compute pipelining groups: dense fields split into ~0.25 GB groups (3..12; measured r02:
         # cfg2 3 groups 147 vs 5 groups 144, cfg5 12 groups 181 vs 5 groups 167 Mcell-steps/s); the
         # detonation fields run as one call (splitting them splits the heavy-first schedule)
         field_bytes = sum(b.ncells * (3 + b.Y.shape[0]) * 8 for b in wl.boxes)
         chunks = args.e2e_chunks if args.e2e_chunks > 0 else \
-            (int(min(12, max(3, round(field_bytes / 0.5e9)))) if args.config in ("cfg2", "cfg2b", "cfg5") else 1)
+            (int(min(12, max(3, round(field_bytes / 0.25e9)))) if args.config in ("cfg2", "cfg2b", "cfg5") else 1)
         hr = HostRunner(chem, sets[0], wl.calls, chunks=chunks)
         for k in range(2):
             hr.load_inputs(sets[k % len(sets)])
@@ -675,22 +675,24 @@ def ours(args):
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
-        d2h_steps = []
+        d2h_steps, h2d_steps = [], []
         for k in range(args.steps):
             hr.load_inputs(sets[k % len(sets)])       # host memcpy into the pinned slab, untimed
             e_ev[k][0].record()
             hr.step(args.rtol, args.atol)
             e_ev[k][1].record()
             d2h_steps.append(hr.d2h_bytes)
+            h2d_steps.append(hr.h2d_bytes)
         torch.cuda.synchronize()
         te = sum(a.elapsed_time(b) for a, b in e_ev) / 1e3
         if world > 1:
             from paper_2510_23993_b200 import sharding
             te = float(sharding.reduce_stats([te], "max")[0])
         e2e = {"value": res["tot_cs"] * args.steps / te / 1e6, "unit": "Mcell-steps/s",
-               "h2d_bytes_per_step": hr.h2d_bytes, "d2h_bytes_per_step": float(np.mean(d2h_steps)),
-               "d2h_note": "results of the boxes the step touched (box_cost > 0); an untouched box's host "
-                           f"T, Y are already its outputs (full field {hr.d2h_bytes_full} B)",
+               "h2d_bytes_per_step": float(np.mean(h2d_steps)), "d2h_bytes_per_step": float(np.mean(d2h_steps)),
+               "copy_note": "H2D: every box's T, then rho/e/Y of boxes with active cells (chem_box_active) on the "
+                            "unpipelined path, the whole slab on the pipelined one; D2H: T, Y of the boxes the step "
+                            f"touched (box_cost > 0) (full field: {hr.h2d_bytes_full} B in, {hr.d2h_bytes_full} B out)",
                "copy_compute_chunks": chunks if hr.pipelined else 1,
                "inputs": f"two alternating {wl.evolve}ed host sets" if len(sets) > 1 else "pristine host inputs"}
         del hr, sets

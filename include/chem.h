@@ -221,7 +221,16 @@ int chem_integrate_boxes(chem_ctx* ctx, int32_t nboxes, const chem_box* boxes, d
 int chem_cell_status(chem_ctx* ctx, const void* ws, size_t ws_bytes, int64_t first, int64_t n,
                      int8_t* status, int32_t* substeps, void* stream);
 
-/* Activity trace (App. B: "the number of active cells after each integration step
+/* Caller-side helper for host-resident fields: active[b] (DEVICE int32 [nboxes], caller-owned) = the
+ * cells of box b that the gate of Alg. 3 §1 would integrate (T >= T_min and not solid), read
+ * from the boxes' T (and solid) only; rho, e and Y are not read, so a caller may move them to the device
+ * only for boxes with active[b] > 0 before chem_integrate_boxes (gated cells are never read or written).
+ * ws: a workspace of >= chem_workspace_bytes(ctx, 0, nboxes) bytes (its box table is overwritten).
+ * Synchronises `stream` before returning. */
+int chem_box_active(chem_ctx* ctx, int32_t nboxes, const chem_box* boxes, int32_t* active, void* ws,
+                    size_t ws_bytes, void* stream);
+
+/* Activity trace (App. B/* Activity trace (App. B: "the number of active cells after each integration step
  * for every grid").  trace: DEVICE int32 [rows][nboxes] owned by the caller; subsequent
  * chem_integrate* calls on this ctx write row 0 = active cells per box after the gate and row i =
  * active cells per box after bulk launch i (i < rows; each launch is K_max attempted substeps per

@@ -269,6 +269,28 @@ class Chem:
         self.last_stats = st.to_dict()
         return self.last_stats
 
+    def box_active(self, boxes):
+        """int32 CUDA tensor [nboxes]: cells of each box the gate would integrate (chem_box_active; reads
+        only T and solid)."""
+        nb = len(boxes)
+        arr = (_b.ChemBox * nb)()
+        for i, bx in enumerate(boxes):
+            _check(bx.T, "T", n=bx.ncells, device=self.device)
+            if bx.solid is not None:
+                _check(bx.solid, "solid", torch.uint8, n=bx.ncells, device=self.device)
+            arr[i].T = bx.T.data_ptr()
+            arr[i].solid = bx.solid.data_ptr() if bx.solid is not None else None
+            arr[i].ncells = bx.ncells
+            arr[i].ld = bx.ncells
+            arr[i].dt = float(bx.dt) if bx.dt > 0 else 1.0
+        nbytes = self.lib.chem_workspace_bytes(self._h, 0, nb)
+        if getattr(self, "_ws_small", None) is None or self._ws_small.numel() < nbytes:
+            self._ws_small = torch.zeros(max(nbytes, 1), dtype=torch.uint8, device=self.device)
+        out = torch.empty(nb, dtype=torch.int32, device=self.device)
+        self._call(self.lib.chem_box_active(self._h, nb, arr, _ptr(out), _ptr(self._ws_small), self._ws_small.numel(),
+                                            self._stream()))
+        return out
+
     def cell_status(self, n=None, first=0, substeps=False):
         """int8 CUDA tensor of CHEM_CELL_* codes for global cells [first, first + n) of
         the last integrate / integrate_boxes call (boxes numbered in call order); with
@@ -288,18 +310,20 @@ class Chem:
 class HostRunner:
     """End-to-end public-API path for host-resident data (the bench's `e2e` leg): pinned host
     buffers -> H2D copies -> chem_integrate_boxes -> D2H of (T, Y), in place on the host like the
-    device API: each group's pinned slab [rho_*][e_*][T_*][Y_*] is copied to the device in one H2D
-    copy and its [T_*][Y_*] results come back into the same slab.  Only boxes the step touched
-    (box_cost > 0: at least one active cell) are copied back; an untouched box's host T, Y are already
-    its outputs (gated cells are bitwise untouched).
+    device API: each group's pinned slab [rho_*][e_*][T_*][Y_*] goes to the device and its [T_*][Y_*]
+    results come back into the same slab.  Gated cells are never read or written, so
+    only boxes the step touched (box_cost > 0) are copied back - an untouched box's host T, Y are
+    already its outputs - and, on the unpipelined path, every box's T goes over first and rho, e, Y
+    follow only for boxes the gate finds active (chem_box_active).
 
     With a single fused call per step, the boxes are processed in `chunks` groups through three
     CUDA streams so that the H2D copy of group i+1 and the D2H copy of group i-1 run on the copy
     engines while group i integrates (the host blocks inside chem_integrate_boxes only on the
     compute stream's counters)."""
 
-    def __init__(self, chem: Chem, host_boxes, calls=None, chunks=4):
+    def __init__(self, chem: Chem, host_boxes, calls=None, chunks=4, selective=True):
         self.chem = chem
+        self.selective = selective      # unpipelined path: H2D of rho, e, Y only for boxes with active cells
         self.calls = calls or [list(range(len(host_boxes)))]
         dev = chem.device
         nb = len(host_boxes)
@@ -336,7 +360,8 @@ class HostRunner:
                 o = [o[0] + ni, o[1] + ni, o[2] + ni, o[3] + ni * si]
             self.slabs.append((h, d, 2 * tot))
         self.load_inputs(host_boxes)
-        self.h2d_bytes = sum(s_[0].numel() * 8 for s_ in self.slabs)
+        self.h2d_bytes_full = sum(s_[0].numel() * 8 for s_ in self.slabs)
+        self.h2d_bytes = self.h2d_bytes_full   # of the last step
         self.d2h_bytes_full = sum((s_[0].numel() - s_[2]) * 8 for s_ in self.slabs)
         self.d2h_bytes = 0                  # of the last step (touched boxes only)
 
@@ -361,6 +386,10 @@ class HostRunner:
     def _h2d_group(self, g):
         h, d, _ = self.slabs[g]
         d.copy_(h, non_blocking=True)
+
+    def _h2d_full(self, g):
+        self._h2d_group(g)
+        return self.slabs[g][0].numel() * 8
 
     def _d2h_boxes(self, boxes):
         """D2H of the [T][Y] results of `boxes` into their slabs: one copy per group when every box
@@ -388,9 +417,35 @@ class HostRunner:
         touched = [i for i, c in zip(ids, cost.cpu().tolist()) if c > 0]   # the call has synchronised
         return st, touched
 
+    def _h2d_active(self, g):
+        """Selective H2D of group g: every box's T first, then rho, e and Y only of the boxes whose gate
+        finds active cells (chem_box_active) - the kernels never read a gated cell's rho, e or Y."""
+        h, d, t0 = self.slabs[g]
+        tot = t0 // 2
+        d[2 * tot:3 * tot].copy_(h[2 * tot:3 * tot], non_blocking=True)
+        grp = self.groups[g]
+        act = self.box_active([self.dev_boxes[i] for i in grp])
+        nbytes = tot * 8
+        if all(a > 0 for a in act):
+            d[:2 * tot].copy_(h[:2 * tot], non_blocking=True)
+            d[3 * tot:].copy_(h[3 * tot:], non_blocking=True)
+            return nbytes + (h.numel() - tot) * 8
+        for i, a in zip(grp, act):
+            if a > 0:
+                _, to, n, yo, ny = self.ranges[i]
+                ro, eo = to - 2 * tot, to - tot
+                d[ro:ro + n].copy_(h[ro:ro + n], non_blocking=True)
+                d[eo:eo + n].copy_(h[eo:eo + n], non_blocking=True)
+                d[yo:yo + ny].copy_(h[yo:yo + ny], non_blocking=True)
+                nbytes += (2 * n + ny) * 8
+        return nbytes
+
+    def box_active(self, boxes):
+        return self.chem.box_active(boxes).cpu().tolist()
+
     def step(self, rtol, atol):
         if not self.pipelined:
-            self._h2d_group(0)
+            self.h2d_bytes = self._h2d_active(0) if self.selective else self._h2d_full(0)
             st, touched = [], set()
             for c in self.calls:
                 s_, t_ = self._call(c, rtol, atol)

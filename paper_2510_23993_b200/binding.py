@@ -73,7 +73,7 @@ class ChemStats(ctypes.Structure):
 # every symbol include/chem.h declares (checked by tests/test_cabi.py on CPU)
 EXPORTED = ("chem_default_opts", "chem_init", "chem_finalize", "chem_strerror", "chem_structure_name",
             "chem_set_opts", "chem_workspace_bytes", "chem_rates", "chem_integrate", "chem_integrate_boxes",
-            "chem_temperature", "chem_energy", "chem_jacobian", "chem_rhs", "chem_set_trace", "chem_internal_energy", "chem_cell_status")
+            "chem_temperature", "chem_energy", "chem_jacobian", "chem_rhs", "chem_set_trace", "chem_internal_energy", "chem_cell_status", "chem_box_active")
 
 _lib = None
 
@@ -110,7 +110,8 @@ def load_library():
     lib.chem_set_trace.argtypes = [P, P, I32]
     lib.chem_internal_energy.argtypes = [P, I64, I64, P, P, P]
     lib.chem_cell_status.argtypes = [P, P, ctypes.c_size_t, I64, I64, P, P, P]
-    for f in ("chem_cell_status", "chem_init", "chem_set_opts", "chem_set_trace", "chem_internal_energy", "chem_rates", "chem_rhs", "chem_jacobian", "chem_temperature",
+    lib.chem_box_active.argtypes = [P, I32, P, P, P, ctypes.c_size_t, P]
+    for f in ("chem_box_active", "chem_cell_status", "chem_init", "chem_set_opts", "chem_set_trace", "chem_internal_energy", "chem_rates", "chem_rhs", "chem_jacobian", "chem_temperature",
               "chem_energy", "chem_integrate", "chem_integrate_boxes"):
         getattr(lib, f).restype = ctypes.c_int
     _lib = lib

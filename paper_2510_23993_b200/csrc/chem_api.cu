@@ -545,6 +545,36 @@ int chem_cell_status(chem_ctx* c, const void* ws, size_t ws_bytes, int64_t first
     return cuda_fail(c, cudaGetLastError());
 }
 
+int chem_box_active(chem_ctx* c, int32_t nboxes, const chem_box* boxes, int32_t* active, void* ws, size_t ws_bytes,
+                    void* stream)
+{
+    CHEM_PRE(c);
+    if (nboxes < 1 || !boxes || !active || !ws) return CHEM_EINVAL;
+    for (int b = 0; b < nboxes; ++b)
+        if (boxes[b].ncells < 0 || (boxes[b].ncells > 0 && !boxes[b].T)) return CHEM_EINVAL;
+    if (ws_bytes < ws_layout(0, nboxes).total) return CHEM_ENOWS;
+    if (ensure_host_boxes(c, nboxes) != CHEM_OK) return CHEM_ECUDA;
+    cudaStream_t s = (cudaStream_t)stream;
+    int64_t maxn = 0;
+    for (int b = 0; b < nboxes; ++b) {
+        const chem_box& x = boxes[b];
+        c->h_boxes[b] = DevBox{x.rho, x.e, x.T, x.Y, x.solid, x.ncells, x.ld, x.dt};
+        maxn = std::max(maxn, (int64_t)x.ncells);
+    }
+    char* base = static_cast<char*>(ws);
+    const WsLayout W = ws_layout(0, nboxes);
+    cudaError_t e;
+    if ((e = cudaMemcpyAsync(base + W.boxes, c->h_boxes, sizeof(DevBox) * nboxes, cudaMemcpyHostToDevice, s)) !=
+            cudaSuccess ||
+        (e = cudaMemsetAsync(active, 0, sizeof(int32_t) * nboxes, s)) != cudaSuccess)
+        return cuda_fail(c, e);
+    const int slices = (int)std::max<int64_t>(1, std::min<int64_t>(64, (maxn + 4095) / 4096));
+    k_box_active<kStreamBS><<<dim3(nboxes, slices), kStreamBS, 0, s>>>(reinterpret_cast<const DevBox*>(base + W.boxes),
+                                                                      c->opts.T_min, active);
+    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(c, e);
+    return cuda_fail(c, cudaStreamSynchronize(s));   // the pinned box table is reused by the next call
+}
+
 int chem_integrate(chem_ctx* c, int64_t n, int64_t ld, const double* rho, const double* e, double* T, double* Y,
                    const uint8_t* solid, double dt, double rtol, double atol, void* ws, size_t ws_bytes,
                    chem_stats* stats, void* stream)

@@ -872,6 +872,21 @@ __global__ void __launch_bounds__(BS) k_integrate(const __grid_constant__ Params
     flush_counters(L, cnt);
 }
 
+// Caller-side helper (chem_box_active): active cells per box under the gate of Alg. 3 §1 (T >= T_min and
+// not solid), without touching the workspace: lets a host-buffer caller move only the boxes a call can
+// touch.  grid = (nboxes, slices); reads 8 B (+1 B solid) per cell.
+template <int BS>
+__global__ void __launch_bounds__(BS) k_box_active(const DevBox* __restrict__ boxes, double T_min, int32_t* active)
+{
+    const DevBox bx = boxes[blockIdx.x];
+    int cnt = 0;
+    for (int64_t i = (int64_t)blockIdx.y * BS + threadIdx.x; i < bx.ncells; i += (int64_t)gridDim.y * BS)
+        cnt += (bx.T[i] >= T_min && !(bx.solid && bx.solid[i])) ? 1 : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(&active[blockIdx.x], cnt);
+}
+
 // A11 per-cell outcome of the last call: workspace state byte -> CHEM_CELL_* code
 // (0 untouched, 1 done, 2 unfinished, -1 failed; a cell still FRESH/RUNNING, which no completed call
 // leaves, reads as failed), and the cell's attempted substeps of the call.  HBM-bound.

@@ -351,6 +351,10 @@ def test_host_runner_matches_device_path(chem, doc, chunks):
     torch.cuda.synchronize()
     assert hr.d2h_bytes == 5 * 512 * (1 + len(doc["species"])) * 8
     assert torch.equal(hr.out_T[0], cold["T"]) and torch.equal(hr.out_Y[0], cold["Y"])
+    if not hr.pipelined:      # selective H2D: the cold box sends its T only
+        assert hr.h2d_bytes == 6 * 512 * 8 + 5 * 512 * (2 + len(doc["species"])) * 8
+    act = chem.box_active(hr.dev_boxes).cpu().tolist()
+    assert act[0] == 0 and all(a == 512 for a in act[1:])
     del rng
 
 
