@@ -490,3 +490,36 @@ def test_budget_equivalence_lpt_vs_alg3(ora):
     for r in res[1:]:
         assert np.array_equal(r[0], res[0][0]) and np.array_equal(r[1], res[0][1])
         assert np.array_equal(r[2], res[0][2]) and r[3:] == res[0][3:]
+
+
+def test_cell_status_multibox_and_box_active(ora):
+    """chem_cell_status numbers the cells of a fused call box after box; chem_box_active counts what the
+    gate would integrate per box without touching the workspace; forget_hints clears the cost hints."""
+    from paper_2510_23993_b200 import Box
+    m = ora.m
+    d = synth.cfg1(m.species, m.W, n=300)
+    T0 = d["T"].copy()
+    T0[:100] = 300.0                                   # box 0 entirely cold
+    e = np.array([ora.energy(t, y) for t, y in zip(T0, d["Y"])])
+    ch = Chem("h2air_li2004", device=0, kmax_sparse=4)
+    solid = torch.zeros(100, dtype=torch.uint8, device=DEV)
+    solid[:10] = 1
+    boxes = [Box(to_dev(d["rho"][a:b]), to_dev(e[a:b]), to_dev(T0[a:b]), species_dev(d["Y"][a:b]), 1e-6,
+                 solid if a == 200 else None) for a, b in ((0, 100), (100, 200), (200, 300))]
+    act = ch.box_active(boxes).cpu().tolist()
+    assert act == [0, 100, 90]
+    st = ch.integrate_boxes(boxes, rtol=1e-9, atol=1e-20)
+    status, steps = ch.cell_status(substeps=True)
+    status, steps = status.cpu().numpy(), steps.cpu().numpy()
+    assert len(status) == 300 and st["active0"] == 190
+    assert np.all(status[:100] == 0) and np.all(status[200:210] == 0) and np.all(steps[:100] == 0)
+    assert set(np.unique(status[100:200])) <= {1, 2} and set(np.unique(status[210:])) <= {1, 2}
+    assert (status == 2).sum() == st["n_unfinished"]
+    assert int(steps.sum()) == st["steps_attempted"]
+    part = ch.cell_status(n=50, first=150).cpu().numpy()
+    assert np.array_equal(part, status[150:200])
+    with pytest.raises(Exception):
+        ch.cell_status(n=10, first=295)                # beyond the call's cells
+    ch.forget_hints()
+    st2 = ch.integrate_boxes(boxes, rtol=1e-9, atol=1e-20)
+    assert st2["hint_accuracy"] == -1.0               # no hints after forget_hints
