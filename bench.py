@@ -340,20 +340,26 @@ def timed(wl, args, steps, warmup, dist=None, before=None, clocks=None, rtol=Non
     torch.cuda.synchronize()
     if clocks:
         clocks.start()
+    wall = []
     for k in range(steps):
         wl.prepare(warmup + k)
         if before:
             before()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
         ev[k][0].record()
         st = wl.step(rtol, atol)
         if dist is not None:
             reds.append(step_reductions(st, wl))
         ev[k][1].record()
+        ev[k][1].synchronize()
+        wall.append((time.perf_counter() - t0) * 1e3)   # host wall clock around the step
         stats += st
     torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
     clk = clocks.stop() if clocks else None
+    timed.last_wall_ms = wall
     return [a.elapsed_time(b) for a, b in ev], stats, clk, reds
 
 
@@ -540,6 +546,7 @@ def measure(args, chem, doc, device, rank, world, dist, config, fm, peaks, with_
     import torch
     wl = build_workload(args, chem, doc, device, rank, world, config=config, evolve=args.evolve)
     steps_ms, stats, clk, reds = timed(wl, args, args.steps, args.warmup, dist, clocks=clocks)
+    wall_ms = float(np.median(timed.last_wall_ms))
     t_rank = sum(steps_ms) / 1e3
     t_total, tot_cs = t_rank, float(wl.cell_steps)
     if world > 1:
@@ -549,7 +556,7 @@ def measure(args, chem, doc, device, rank, world, dist, config, fm, peaks, with_
     flops, k_ms, ach = roofline(fm, stats, *peaks)
     res = dict(value=tot_cs * args.steps / t_total / 1e6, ms_per_step=1e3 * t_total / args.steps,
                steps_ms=steps_ms, t_rank=t_rank, stats=stats, flops=flops, k_ms=k_ms, achieved=ach,
-               clocks=clk, reductions=reds[-1] if reds else None, tot_cs=tot_cs)
+               clocks=clk, reductions=reds[-1] if reds else None, tot_cs=tot_cs, wall_ms=wall_ms)
     if with_variants and config != "cfg2" and not args.no_schedules:
         var = {}
         chem_opts0 = dict(schedule_lpt=chem.opts.schedule_lpt)
@@ -778,7 +785,9 @@ def ours(args):
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches, "clocks": res["clocks"],
             "schedules": res.get("schedules"), "production_tolerance": res.get("production_tolerance"),
             "also": also or None,
-            "detail": {"step_ms": res["steps_ms"], "rank0_seconds": res["t_rank"],
+            "detail": {"step_ms": res["steps_ms"], "step_ms_median": float(np.median(res["steps_ms"])),
+                       "step_ms_min": float(np.min(res["steps_ms"])), "step_ms_max": float(np.max(res["steps_ms"])),
+                       "host_wall_ms_per_step": res.get("wall_ms"), "rank0_seconds": res["t_rank"],
                        "k_integrate_ms": res["k_ms"] / args.steps,
                        "integrate_launches": launches_int, "substeps_per_cell_step": att / max(wl_cs, 1),
                        "accepted_per_cell_step": acc / max(wl_cs, 1),
