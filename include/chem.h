@@ -106,7 +106,7 @@ typedef struct {
     int32_t kmax_first;     /* substeps of the first bulk burst of a lockstep call (1: cells that
                                finish in one substep leave before the lockstep bursts); 0: kmax_bulk */
     int32_t schedule_lpt;   /* heavy-first schedule: the active list sorted by predicted cost and run as
-                               one persistent lockstep launch, longest cells first.  Predictions come
+                               one persistent launch with lane refill, longest cells first.  Predictions come
                                from the previous call's per-cell substeps on the same layout (kept in
                                the workspace) or, within the call, from each cell's own state after the
                                first bulk burst (remaining substeps (dt - t)/h).  0 off (Alg. 3);

@@ -836,13 +836,9 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
     if (n_cur > 0) {
         CK(cudaMemsetAsync(L.stats + S_CURSOR, 0, 8, s));
         CK(cudaEventRecord(c->ev[0], s));
-#ifndef CHEM_LPT_FREE
-        if (lpt) {
-            // heavy-first: persistent lockstep blocks (one per SM) with warp-batched refill
-            CK(ops.integrate_lock(c->params.data(), o.method, L, cur, n_cur, o.kmax_sparse, 1, 1, c->num_sms, s));
-        } else
-#endif
         {
+            // the sparse list (sorted heaviest first under the heavy-first schedule) on the free-running
+            // persistent grid with warp-batched lane refill (lockstep blocks cost 2-7 % here, r02t)
             const int grid = std::max(1, std::min<int>(c->num_sms * ops.blocks_per_sm(o.method),
                                                        (int)((n_cur + kIntegrateBS - 1) / kIntegrateBS)));
             CK(ops.integrate(c->params.data(), o.method, L, cur, n_cur, o.kmax_sparse, 1, 1, grid, s));
