@@ -335,6 +335,12 @@ __global__ void __launch_bounds__(BS) k_box_count(LaunchCtx L, const uint32_t* i
 }
 
 // ----------------------------------------------------------------------------- A6/A7/A9 integrate
+// persistent lane refill: idle lanes of a warp with busy lanes wait until this many are idle
+#ifdef CHEM_REFILL_BATCH
+constexpr int kRefillBatch = CHEM_REFILL_BATCH;
+#else
+constexpr int kRefillBatch = 8;
+#endif
 // Per-thread shared memory (stride = block size, conflict-free): the n x n iteration matrix
 // (I/(h gamma) - J, then its LU) and the stored stage vectors K_s (pivot rows stay in registers);
 // n = NSA+1 unknowns (reacting Y_k and T, Eq. 6).  Stiffly accurate methods (RODAS4) do not store
@@ -827,7 +833,7 @@ __global__ void __launch_bounds__(BS) k_integrate(const __grid_constant__ Params
                 const unsigned need = __ballot_sync(FULL, !have && live);
                 if (need == 0) break;
                 const unsigned busy = __ballot_sync(FULL, have);
-                if (busy != 0 && __popc(need) < 8) break;
+                if (busy != 0 && __popc(need) < kRefillBatch) break;
                 const int leader = __ffs(need) - 1;
                 unsigned long long base = 0;
                 if (lane == leader) base = atomicAdd(&L.stats[S_CURSOR], (unsigned long long)__popc(need));
