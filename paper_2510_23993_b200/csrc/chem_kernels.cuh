@@ -335,11 +335,13 @@ __global__ void __launch_bounds__(BS) k_box_count(LaunchCtx L, const uint32_t* i
 }
 
 // ----------------------------------------------------------------------------- A6/A7/A9 integrate
-// persistent lane refill: idle lanes of a warp with busy lanes wait until this many are idle
+// persistent lane refill: idle lanes of a warp with busy lanes wait until this many are idle (round 1
+// batched 8; on the cost-sorted lists of round 2 refilling every idle lane at once is fastest: cfg3
+// 195.8 -> 200.7, cfg5 279.2 -> 294.3 Mcell-steps/s, batches of 2 / 4 in between, r02v)
 #ifdef CHEM_REFILL_BATCH
 constexpr int kRefillBatch = CHEM_REFILL_BATCH;
 #else
-constexpr int kRefillBatch = 8;
+constexpr int kRefillBatch = 1;
 #endif
 // Per-thread shared memory (stride = block size, conflict-free): the n x n iteration matrix
 // (I/(h gamma) - J, then its LU) and the stored stage vectors K_s (pivot rows stay in registers);
