@@ -777,18 +777,9 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
         CK(cudaEventRecord(c->ev[0], s));
         if (lock)
             CK(ops.integrate_lock(c->params.data(), o.method, L, lst, nl, kmax_b, 0, 0, c->num_sms, s));
-#ifdef CHEM_BULK_REFILL
-        else {   // experiment: the burst on the persistent refill grid
-            CK(cudaMemsetAsync(L.stats + S_CURSOR, 0, 8, s));
-            const int grid = std::max(1, std::min<int>(c->num_sms * ops.blocks_per_sm(o.method),
-                                                       (int)((nl + kIntegrateBS - 1) / kIntegrateBS)));
-            CK(ops.integrate(c->params.data(), o.method, L, lst, nl, kmax_b, 1, 0, grid, s));
-        }
-#else
         else
             CK(ops.integrate(c->params.data(), o.method, L, lst, nl, kmax_b, 0, 0,
                              (int)((nl + kIntegrateBS - 1) / kIntegrateBS), s));
-#endif
         CK(cudaEventRecord(c->ev[1], s));
         CK(cudaEventSynchronize(c->ev[1]));
         st.t_bulk_ms += elapsed(c);
