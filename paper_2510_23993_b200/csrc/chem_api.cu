@@ -836,9 +836,14 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
     if (n_cur > 0) {
         CK(cudaMemsetAsync(L.stats + S_CURSOR, 0, 8, s));
         CK(cudaEventRecord(c->ev[0], s));
-        {
-            // the sparse list (sorted heaviest first under the heavy-first schedule) on the free-running
-            // persistent grid with warp-batched lane refill (lockstep blocks cost 2-7 % here, r02t)
+        if (st.lpt == 1) {
+            // heavy-first on the previous call's hints: the whole active list, light cells included, as
+            // persistent lockstep blocks (one per SM) with lane refill - a free-running refill grid costs
+            // 1-substep cells their coalesced loads (cfg5 at the production tolerance 507 vs 345, r02)
+            CK(ops.integrate_lock(c->params.data(), o.method, L, cur, n_cur, o.kmax_sparse, 1, 1, c->num_sms, s));
+        } else {
+            // the sparse list (after the bursts; sorted heaviest first under the in-call prediction) on
+            // the free-running persistent grid with lane refill (lockstep costs 2-7 % here, r02t)
             const int grid = std::max(1, std::min<int>(c->num_sms * ops.blocks_per_sm(o.method),
                                                        (int)((n_cur + kIntegrateBS - 1) / kIntegrateBS)));
             CK(ops.integrate(c->params.data(), o.method, L, cur, n_cur, o.kmax_sparse, 1, 1, grid, s));
