@@ -786,6 +786,7 @@ __global__ void __launch_bounds__(BS) k_integrate(const __grid_constant__ Params
     bool live = true;     // this thread may still take a cell
     bool first = true;
     int64_t tile = blockIdx.x;
+    int64_t next_idx = 0;  // free-running bulk: the list entry this thread took last
     // one attempted substep of the lane's cell and its write-back when the cell leaves the launch
     auto substep = [&]() {
         {   // SIMT efficiency statistic: the lowest lane executing this substep counts one warp substep
@@ -857,9 +858,13 @@ __global__ void __launch_bounds__(BS) k_integrate(const __grid_constant__ Params
             if (!have) continue;
         } else {
             while (!have && live) {
-                const int64_t idx = !first ? n_ids : LOCK ? tile * BS + threadIdx.x   // persistent tiles
-                                                          : (int64_t)blockIdx.x * BS + threadIdx.x;
+                // LOCK: persistent tiles of the block; free-running: a grid-stride walk per thread (a
+                // grid smaller than the list makes the launch persistent: per-block setup paid once)
+                const int64_t idx = LOCK ? (!first ? n_ids : tile * BS + threadIdx.x)
+                                         : (first ? (int64_t)blockIdx.x * BS + threadIdx.x
+                                                  : next_idx + (int64_t)gridDim.x * BS);
                 first = false;
+                next_idx = idx;
                 if (idx >= n_ids) { live = false; break; }
                 take(idx);
             }
