@@ -777,18 +777,9 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
         CK(cudaEventRecord(c->ev[0], s));
         if (lock)
             CK(ops.integrate_lock(c->params.data(), o.method, L, lst, nl, kmax_b, 0, 0, c->num_sms, s));
-        else {
-#ifdef CHEM_BULK_PERSIST
-            // experiment: persistent bulk grid (CHEM_BULK_PERSIST waves of resident blocks), each thread
-            // walking the list with a grid stride
-            const int64_t blocks = (nl + kIntegrateBS - 1) / kIntegrateBS;
-            const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(
-                blocks, (int64_t)CHEM_BULK_PERSIST * c->num_sms * ops.blocks_per_sm(o.method)));
-#else
-            const int grid = (int)((nl + kIntegrateBS - 1) / kIntegrateBS);
-#endif
-            CK(ops.integrate(c->params.data(), o.method, L, lst, nl, kmax_b, 0, 0, grid, s));
-        }
+        else
+            CK(ops.integrate(c->params.data(), o.method, L, lst, nl, kmax_b, 0, 0,
+                             (int)((nl + kIntegrateBS - 1) / kIntegrateBS), s));
         CK(cudaEventRecord(c->ev[1], s));
         CK(cudaEventSynchronize(c->ev[1]));
         st.t_bulk_ms += elapsed(c);

@@ -28,8 +28,9 @@ def regions(fname):
 def main(lib, name):
     d = tempfile.mkdtemp()
     subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(lib)], cwd=d, capture_output=True)
-    cubin = [f for f in os.listdir(d) if f.endswith(".cubin")][0]
-    txt = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(d, cubin)], capture_output=True, text=True).stdout
+    txt = ""
+    for cubin in sorted(f for f in os.listdir(d) if f.endswith(".cubin")):   # one per translation unit
+        txt += subprocess.run(["nvdisasm", "-g", "-c", os.path.join(d, cubin)], capture_output=True, text=True).stdout
     lines = txt.splitlines()
     inside = False
     cur = None
