@@ -1,7 +1,7 @@
 #!/bin/bash
 # Round-2 evidence in one gpurun call.  Output: gpurun_out/final_* (copied to profiles/ afterwards).
 set -u
-T=final
+T=${T:-final}
 mkdir -p gpurun_out
 timeout 1800 python -m pytest tests -m gpu -q -s --durations=8 > gpurun_out/${T}_tests_full.txt 2>&1
 grep -E "passed|failed|self-convergence|gap at" gpurun_out/${T}_tests_full.txt | tail -8
