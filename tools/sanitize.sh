@@ -1,6 +1,6 @@
 #!/bin/bash
 # compute-sanitizer memcheck / racecheck / synccheck / initcheck over a small chem_integrate
-# (cfg1c cells in two boxes: the free-running, lockstep and heavy-first launches, a budget-capped call).  Output: gpurun_out/sanitize_*.txt
+# (cfg1c cells in two boxes: the free-running, lockstep, cross-call and in-call heavy-first launches, budget-capped calls).  Output: gpurun_out/sanitize_*.txt
 mkdir -p gpurun_out
 cat > /tmp/san_case.py <<'PY'
 import sys, os
@@ -12,7 +12,7 @@ m = load_mechanism("h2air_li2004")
 d = synth.cfg1c(m.species, m.W)
 idx = np.arange(0, 4096, 64)
 dev = torch.device("cuda", 0)
-for lock, lpt, ksp in ((0, 0, 100000), (1, 0, 100000), (0, 1, 100000), (0, 1, 7), (0, 0, 7)):
+for lock, lpt, ksp in ((0, 0, 100000), (1, 0, 100000), (0, 1, 100000), (0, 1, 7), (0, 0, 7), (0, 3, 100000), (0, 3, 7), (2, 2, 100000)):
     ch = Chem("h2air_li2004", device=0, kmax_bulk=3, n_active_star=16, lockstep=lock, schedule_lpt=lpt,
               kmax_sparse=ksp)
     T = torch.tensor(d["T"][idx], device=dev)
