@@ -319,7 +319,8 @@ class HostRunner:
     With a single fused call per step, the boxes are processed in `chunks` groups through three
     CUDA streams so that the H2D copy of group i+1 and the D2H copy of group i-1 run on the copy
     engines while group i integrates (the host blocks inside chem_integrate_boxes only on the
-    compute stream's counters)."""
+    compute stream's counters, which the library reads through mapped memory, not a copy engine);
+    a pipelined group returns the results of all its boxes."""
 
     def __init__(self, chem: Chem, host_boxes, calls=None, chunks=4, selective=True):
         self.chem = chem
@@ -411,7 +412,13 @@ class HostRunner:
                 nbytes += (n + ny) * 8
         return nbytes
 
-    def _call(self, ids, rtol, atol):
+    def _call(self, ids, rtol, atol, touched_only=True):
+        if not touched_only:
+            # pipelined groups: every box's results come back.  Reading box_cost here would put a
+            # copy-engine D2H on the compute stream, and the next call's commands would then wait for
+            # the group D2H queued meanwhile on the copy stream (tools/e2e_timeline.py)
+            st = self.chem.integrate_boxes([self.dev_boxes[i] for i in ids], rtol=rtol, atol=atol)
+            return st, list(ids)
         cost = torch.zeros(len(ids), dtype=torch.float64, device=self.chem.device)
         st = self.chem.integrate_boxes([self.dev_boxes[i] for i in ids], rtol=rtol, atol=atol, box_cost=cost)
         touched = [i for i, c in zip(ids, cost.cpu().tolist()) if c > 0]   # the call has synchronised
@@ -468,7 +475,7 @@ class HostRunner:
                     self._h2d_group(g + 1)
                     ev_in[g + 1].record(self.s_h2d)
             comp.wait_event(ev_in[g])
-            s_, touched = self._call(idx, rtol, atol)
+            s_, touched = self._call(idx, rtol, atol, touched_only=False)
             st.append(s_)
             done = torch.cuda.Event()
             done.record(comp)

@@ -313,9 +313,13 @@ struct chem_ctx {
     int num_sms = 148;
     int sticky = 0;
     int32_t h_cap = 0;
-    DevBox* h_boxes = nullptr;        // pinned
-    int64_t* h_start = nullptr;       // pinned
-    unsigned long long* h_stats = nullptr;  // pinned [S_NSTATS]
+    DevBox* h_boxes = nullptr;        // pinned, mapped (d_boxes: its device alias)
+    int64_t* h_start = nullptr;       // pinned, mapped
+    unsigned long long* h_stats = nullptr;  // pinned, mapped [S_NSTATS]
+    DevBox* d_boxes = nullptr;
+    int64_t* d_start = nullptr;
+    unsigned long long* d_stats = nullptr;
+    unsigned long long* d_sig = nullptr;
     cudaEvent_t ev[2] = {nullptr, nullptr};
     int32_t* trace = nullptr;        // device [trace_rows][nboxes] activity trace (App. B), or null
     int32_t trace_rows = 0;
@@ -335,6 +339,18 @@ int cuda_fail(chem_ctx* c, cudaError_t e)
     return CHEM_ECUDA;
 }
 
+// Pinned host buffer mapped into the device address space (h: host pointer, d: its device alias).
+template <class T>
+bool alloc_mapped(T*& h, T*& d, size_t count)
+{
+    h = nullptr;
+    d = nullptr;
+    if (cudaHostAlloc((void**)&h, sizeof(T) * count, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess)
+        return false;
+    if (cudaHostGetDevicePointer((void**)&d, (void*)h, 0) != cudaSuccess) return false;
+    return true;
+}
+
 int ensure_host_boxes(chem_ctx* c, int32_t nb)
 {
     if (nb <= c->h_cap) return CHEM_OK;
@@ -343,10 +359,47 @@ int ensure_host_boxes(chem_ctx* c, int32_t nb)
     c->h_boxes = nullptr;
     c->h_start = nullptr;
     int cap = std::max(nb, 64);
-    if (cudaMallocHost(&c->h_boxes, sizeof(DevBox) * cap) != cudaSuccess) return CHEM_ECUDA;
-    if (cudaMallocHost(&c->h_start, sizeof(int64_t) * (cap + 1)) != cudaSuccess) return CHEM_ECUDA;
+    if (!alloc_mapped(c->h_boxes, c->d_boxes, cap)) return CHEM_ECUDA;
+    if (!alloc_mapped(c->h_start, c->d_start, cap + 1)) return CHEM_ECUDA;
     c->h_cap = cap;
     return CHEM_OK;
+}
+
+// The call's bookkeeping transfers (box table in, counters out; a few hundred bytes to ~100 KB) and its
+// small memsets run as kernels on the caller's stream, through the mapped buffers above, never as
+// copy-engine operations: a stream whose previous command was a cudaMemcpyAsync / cudaMemsetAsync lets
+// its next command start only when the copy engine is through with every larger copy queued on it by
+// then, so a host-buffer caller that overlaps the D2H of one box group with the next call (HostRunner)
+// saw each call wait for the previous group's whole D2H (tools/e2e_timeline.py, profiles/r02_e2e_timeline_*).
+__global__ void k_copy_words(const unsigned long long* __restrict__ src, unsigned long long* __restrict__ dst,
+                             int64_t n)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+}
+
+__global__ void k_zero_bytes(unsigned char* __restrict__ dst, int64_t n)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = 0;
+}
+
+cudaError_t copy_words(void* dst, const void* src, size_t bytes, cudaStream_t s)   // bytes % 8 == 0
+{
+    const int64_t n = (int64_t)(bytes / 8);
+    if (n == 0) return cudaSuccess;
+    const int grid = (int)std::min<int64_t>(64, (n + 255) / 256);
+    k_copy_words<<<grid, 256, 0, s>>>(static_cast<const unsigned long long*>(src),
+                                       static_cast<unsigned long long*>(dst), n);
+    return cudaGetLastError();
+}
+
+cudaError_t zero_bytes(void* dst, size_t bytes, cudaStream_t s)
+{
+    if (bytes == 0) return cudaSuccess;
+    const int grid = (int)std::min<int64_t>(256, ((int64_t)bytes + 255) / 256);
+    k_zero_bytes<<<grid, 256, 0, s>>>(static_cast<unsigned char*>(dst), (int64_t)bytes);
+    return cudaGetLastError();
 }
 
 float elapsed(chem_ctx* c)
@@ -424,8 +477,7 @@ int chem_init(const chem_mech_desc* mech, const chem_opts* opts, int device, che
     c->params.resize(ops->params_size);
     ops->fill(mech, c->params.data());
     cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
-    if (cudaMallocHost(&c->h_stats, sizeof(unsigned long long) * S_NSTATS) != cudaSuccess ||
-        cudaMallocHost(&c->h_sig, sizeof(unsigned long long) * 6) != cudaSuccess ||
+    if (!alloc_mapped(c->h_stats, c->d_stats, S_NSTATS) || !alloc_mapped(c->h_sig, c->d_sig, 6) ||
         cudaEventCreate(&c->ev[0]) != cudaSuccess || cudaEventCreate(&c->ev[1]) != cudaSuccess ||
         ensure_host_boxes(c, 64) != CHEM_OK) {
         chem_finalize(c);
@@ -564,9 +616,8 @@ int chem_box_active(chem_ctx* c, int32_t nboxes, const chem_box* boxes, int32_t*
     char* base = static_cast<char*>(ws);
     const WsLayout W = ws_layout(0, nboxes);
     cudaError_t e;
-    if ((e = cudaMemcpyAsync(base + W.boxes, c->h_boxes, sizeof(DevBox) * nboxes, cudaMemcpyHostToDevice, s)) !=
-            cudaSuccess ||
-        (e = cudaMemsetAsync(active, 0, sizeof(int32_t) * nboxes, s)) != cudaSuccess)
+    if ((e = copy_words(base + W.boxes, c->d_boxes, sizeof(DevBox) * nboxes, s)) != cudaSuccess ||
+        (e = zero_bytes(active, sizeof(int32_t) * nboxes, s)) != cudaSuccess)
         return cuda_fail(c, e);
     const int slices = (int)std::max<int64_t>(1, std::min<int64_t>(64, (maxn + 4095) / 4096));
     k_box_active<kStreamBS><<<dim3(nboxes, slices), kStreamBS, 0, s>>>(reinterpret_cast<const DevBox*>(base + W.boxes),
@@ -662,10 +713,10 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
         if ((e = (x)) != cudaSuccess) return cuda_fail(c, e); \
     } while (0)
 
-    CK(cudaMemcpyAsync(base + W.boxes, c->h_boxes, sizeof(DevBox) * nboxes, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(base + W.start, c->h_start, sizeof(int64_t) * (nboxes + 1), cudaMemcpyHostToDevice, s));
-    CK(cudaMemsetAsync(L.stats, 0, S_SIG0 * 8, s));   // the layout signature slots persist across calls
-    if (box_cost) CK(cudaMemsetAsync(box_cost, 0, sizeof(double) * nboxes, s));
+    CK(copy_words(base + W.boxes, c->d_boxes, sizeof(DevBox) * nboxes, s));
+    CK(copy_words(base + W.start, c->d_start, sizeof(int64_t) * (nboxes + 1), s));
+    CK(zero_bytes(L.stats, S_SIG0 * 8, s));   // the layout signature slots persist across calls
+    if (box_cost) CK(zero_bytes(box_cost, sizeof(double) * nboxes, s));
     if (total == 0) {
         CK(cudaStreamSynchronize(s));
         if (stats) *stats = st;
@@ -673,7 +724,7 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
     }
 
     auto read_count = [&](int64_t& v) -> cudaError_t {
-        cudaError_t r = cudaMemcpyAsync(c->h_stats, L.stats, S_NSTATS * 8, cudaMemcpyDeviceToHost, s);
+        cudaError_t r = copy_words(c->d_stats, L.stats, S_NSTATS * 8, s);
         if (r != cudaSuccess) return r;
         r = cudaStreamSynchronize(s);
         v = (int64_t)c->h_stats[S_COUNT_ACTIVE];
@@ -693,7 +744,7 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
     st.active0 = n_active;
     const bool tracing = c->trace && c->trace_rows > 0;
     if (tracing) {
-        CK(cudaMemsetAsync(c->trace, 0, sizeof(int32_t) * (size_t)c->trace_rows * nboxes, s));
+        CK(zero_bytes(c->trace, sizeof(int32_t) * (size_t)c->trace_rows * nboxes, s));
         if (n_active > 0) {
             k_box_count<kStreamBS><<<grid_for(n_active, kStreamBS), kStreamBS, 0, s>>>(L, ids0, n_active, c->trace);
             CK(cudaGetLastError());
@@ -723,7 +774,7 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
     c->h_sig[4] = 0;
     c->h_sig[5] = history ? 1 : 0;
     static_assert(S_HINT_MIN == S_SIG2 + 1 && S_HINT_VALID == S_SIG2 + 3, "signature + hint slots are contiguous");
-    CK(cudaMemcpyAsync(L.stats + S_SIG0, c->h_sig, 6 * sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
+    CK(copy_words(L.stats + S_SIG0, c->d_sig, 6 * sizeof(unsigned long long), s));
     const uint64_t pred_total = c->h_stats[S_PRED_TOTAL], pred_heavy = c->h_stats[S_PRED_HEAVY];
     const uint64_t pred_max = c->h_stats[S_PRED_MAX];
     const bool eligible = n_active > 0 && o.method != CHEM_METHOD_EXPLICIT;
@@ -784,7 +835,7 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
         CK(cudaEventSynchronize(c->ev[1]));
         st.t_bulk_ms += elapsed(c);
         CK(cudaEventRecord(c->ev[0], s));
-        CK(cudaMemsetAsync(L.stats + S_COUNT_ACTIVE, 0, 8, s));
+        CK(zero_bytes(L.stats + S_COUNT_ACTIVE, 8, s));
         k_compact<kStreamBS><<<grid_for(nl, kStreamBS), kStreamBS, 0, s>>>(L, lst, nl, nxt);
         CK(cudaGetLastError());
         CK(cudaEventRecord(c->ev[1], s));
@@ -807,7 +858,7 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
         if (predict && st.bulk_iters == 1 && n_cur > 0 && (o.schedule_lpt == 3 || n_cur > wave)) {
             // heavy-first on in-call predictions: the remaining substeps (dt - t)/h of every cell still
             // active after the first burst; skewed (max > 1.5 mean) or forced -> sort, one persistent launch
-            CK(cudaMemsetAsync(L.stats + S_PRED2_TOTAL, 0, 16, s));
+            CK(zero_bytes(L.stats + S_PRED2_TOTAL, 16, s));
             k_predict<kStreamBS><<<grid_for(n_cur, kStreamBS), kStreamBS, 0, s>>>(L, cur, n_cur, key0);
             CK(cudaGetLastError());
             int64_t dummy;
@@ -834,7 +885,7 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
     // ---- Alg. 3 §3: sparse integration over the index map (persistent, lane refill)
     st.sparse_cells = n_cur;
     if (n_cur > 0) {
-        CK(cudaMemsetAsync(L.stats + S_CURSOR, 0, 8, s));
+        CK(zero_bytes(L.stats + S_CURSOR, 8, s));
         CK(cudaEventRecord(c->ev[0], s));
         if (st.lpt == 1) {
             // heavy-first on the previous call's hints: the whole active list, light cells included, as
@@ -854,7 +905,7 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
         k_box_cost<kStreamBS><<<grid_for(n_active, kStreamBS), kStreamBS, 0, s>>>(L, ids0, n_active, box_cost);
         CK(cudaGetLastError());
     }
-    CK(cudaMemcpyAsync(c->h_stats, L.stats, S_NSTATS * 8, cudaMemcpyDeviceToHost, s));
+    CK(copy_words(c->d_stats, L.stats, S_NSTATS * 8, s));
     CK(cudaStreamSynchronize(s));
     if (n_cur > 0) st.t_sparse_ms = elapsed(c);
     const unsigned long long* hs = c->h_stats;

@@ -341,7 +341,8 @@ def test_host_runner_matches_device_path(chem, doc, chunks):
             assert torch.equal(hr.out_T[i], b.T.cpu()) and torch.equal(hr.out_Y[i], b.Y.cpu())
     assert hr.h2d_bytes == 6 * 512 * (3 + len(doc["species"])) * 8
     assert hr.d2h_bytes == 6 * 512 * (1 + len(doc["species"])) * 8       # every box active
-    # an all-cold box is not copied back: its host data are its outputs already
+    # an all-cold box is not copied back on the unpipelined path: its host data are its outputs already
+    # (a pipelined group returns all its boxes; the cold box's device copy is its input, bitwise)
     cold = dict(host[0])
     cold["T"] = torch.full_like(host[0]["T"], 300.0).pin_memory()
     cold["e"] = chem.energy(cold["T"].to(DEV), host[0]["Y"].to(DEV)).cpu().pin_memory()
@@ -349,7 +350,7 @@ def test_host_runner_matches_device_path(chem, doc, chunks):
     hr.load_inputs(host2)
     hr.step(**GPU_TOL)
     torch.cuda.synchronize()
-    assert hr.d2h_bytes == 5 * 512 * (1 + len(doc["species"])) * 8
+    assert hr.d2h_bytes == (6 if hr.pipelined else 5) * 512 * (1 + len(doc["species"])) * 8
     assert torch.equal(hr.out_T[0], cold["T"]) and torch.equal(hr.out_Y[0], cold["Y"])
     if not hr.pipelined:      # selective H2D: the cold box sends its T only
         assert hr.h2d_bytes == 6 * 512 * 8 + 5 * 512 * (2 + len(doc["species"])) * 8

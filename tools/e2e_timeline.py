@@ -25,6 +25,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="cfg2")
     ap.add_argument("--chunks", type=int, default=3)
+    ap.add_argument("--comp-stream", action="store_true", help="compute on a dedicated stream, not the default")
+    ap.add_argument("--no-wait", action="store_true", help="host-side ev_in.synchronize() instead of stream wait")
+    ap.add_argument("--no-done", action="store_true", help="D2H stream: host sync instead of waiting on `done`")
     a = ap.parse_args()
     argv, sys.argv = sys.argv, [sys.argv[0], "--config", a.config]
     args = bench.parse()
@@ -44,13 +47,18 @@ def main():
     hr.load_inputs(hs)
     ev = {}
 
+    hostt = {}
+
     def mark(name, stream):
         e = torch.cuda.Event(enable_timing=True)
         e.record(stream)
         ev[name] = e
+        hostt[name] = time.perf_counter()
 
-    comp = torch.cuda.current_stream(dev)
-    host = {}
+    comp = torch.cuda.Stream(dev) if a.comp_stream else torch.cuda.current_stream(dev)
+    torch.cuda.set_stream(comp)
+    host = {"comp_stream": int(comp.cuda_stream), "h2d_stream": int(hr.s_h2d.cuda_stream),
+            "d2h_stream": int(hr.s_d2h.cuda_stream)}
     # the pipelined HostRunner.step, with events around each piece (same order of enqueues)
     t0 = time.perf_counter()
     mark("start", comp)
@@ -69,16 +77,21 @@ def main():
                 hr._h2d_group(g + 1)
                 mark(f"h2d{g + 1}_b", hr.s_h2d)
                 ev_in[g + 1].record(hr.s_h2d)
-        comp.wait_event(ev_in[g])
+        mark(f"pre{g}", comp)
+        if a.no_wait:
+            ev_in[g].synchronize()
+        else:
+            comp.wait_event(ev_in[g])
         mark(f"call{g}_a", comp)
         th = time.perf_counter()
-        s_, touched = hr._call(idx, args.rtol, args.atol)
+        s_, touched = hr._call(idx, args.rtol, args.atol, touched_only=False)
         host[f"call{g}_host_ms"] = 1e3 * (time.perf_counter() - th)
         mark(f"call{g}_b", comp)
         done = torch.cuda.Event()
         done.record(comp)
         with torch.cuda.stream(hr.s_d2h):
-            hr.s_d2h.wait_event(done)
+            if not a.no_done:
+                hr.s_d2h.wait_event(done)
             mark(f"d2h{g}_a", hr.s_d2h)
             hr._d2h_boxes(touched)
             mark(f"d2h{g}_b", hr.s_d2h)
@@ -87,8 +100,9 @@ def main():
     torch.cuda.synchronize()
     host["step_host_ms"] = 1e3 * (time.perf_counter() - t0)
     tl = {k: round(ev["start"].elapsed_time(e), 3) for k, e in ev.items()}
+    host["enqueued_at_ms"] = {k: round(1e3 * (v - hostt["start"]), 3) for k, v in hostt.items()}
     print(json.dumps({"config": a.config, "chunks": a.chunks, "groups": [len(g) for g in hr.groups],
-                      "timeline_ms": tl, "host": {k: round(v, 3) for k, v in host.items()}}, indent=1))
+                      "timeline_ms": tl, "host": {k: (round(v, 3) if isinstance(v, float) else v) for k, v in host.items()}}, indent=1))
 
 
 if __name__ == "__main__":
