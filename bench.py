@@ -76,6 +76,8 @@ def parse():
     p.add_argument("--cpu-sample-seconds", type=float, default=15.0)
     p.add_argument("--balance", default="lpt", choices=["lpt", "none"])
     p.add_argument("--e2e-chunks", type=int, default=0, help="e2e copy/compute pipelining groups (0: auto)")
+    p.add_argument("--e2e-taper", type=float, default=2.0,
+                   help="e2e: share of a middle group relative to the first and last groups")
     p.add_argument("--opt", action="append", default=[], metavar="KEY=VAL",
                    help="extra chem_opts field (e.g. kmax_bulk=5, schedule_lpt=0); repeatable")
     p.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
@@ -672,7 +674,7 @@ def ours(args):
         field_bytes = sum(b.ncells * (3 + b.Y.shape[0]) * 8 for b in wl.boxes)
         chunks = args.e2e_chunks if args.e2e_chunks > 0 else \
             (int(min(12, max(3, round(field_bytes / 0.25e9)))) if args.config in ("cfg2", "cfg2b", "cfg5") else 1)
-        hr = HostRunner(chem, sets[0], wl.calls, chunks=chunks)
+        hr = HostRunner(chem, sets[0], wl.calls, chunks=chunks, taper=args.e2e_taper)
         for k in range(2):
             hr.load_inputs(sets[k % len(sets)])
             hr.step(args.rtol, args.atol)
@@ -701,6 +703,7 @@ def ours(args):
                             "unpipelined path, the whole slab on the pipelined one; D2H: T, Y of the boxes the step "
                             f"touched (box_cost > 0) (full field: {hr.h2d_bytes_full} B in, {hr.d2h_bytes_full} B out)",
                "copy_compute_chunks": chunks if hr.pipelined else 1,
+               "taper": args.e2e_taper if hr.pipelined else None,
                "inputs": f"two alternating {wl.evolve}ed host sets" if len(sets) > 1 else "pristine host inputs"}
         del hr, sets
 

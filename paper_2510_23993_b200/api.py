@@ -322,7 +322,7 @@ class HostRunner:
     compute stream's counters, which the library reads through mapped memory, not a copy engine);
     a pipelined group returns the results of all its boxes."""
 
-    def __init__(self, chem: Chem, host_boxes, calls=None, chunks=4, selective=True):
+    def __init__(self, chem: Chem, host_boxes, calls=None, chunks=4, selective=True, taper=2.0):
         self.chem = chem
         self.selective = selective      # unpipelined path: H2D of rho, e, Y only for boxes with active cells
         self.calls = calls or [list(range(len(host_boxes)))]
@@ -331,9 +331,9 @@ class HostRunner:
         self.pipelined = len(self.calls) == 1 and len(self.calls[0]) >= chunks > 1
         if self.pipelined:
             # tapered groups: the first group's H2D and the last group's D2H are the copies nothing
-            # overlaps, so those two groups get half the share of the middle ones
+            # overlaps, so those two groups get 1/taper of the share of the middle ones
             ids = self.calls[0]
-            w = [1.0] + [2.0] * (chunks - 2) + [1.0] if chunks > 2 else [1.0] * chunks
+            w = [1.0] + [float(taper)] * (chunks - 2) + [1.0] if chunks > 2 else [1.0] * chunks
             cuts = np.round(np.cumsum([0.0] + w) / sum(w) * len(ids)).astype(int)
             self.groups = [ids[cuts[g]:cuts[g + 1]] for g in range(chunks) if cuts[g + 1] > cuts[g]]
             self.s_h2d = torch.cuda.Stream(dev)
