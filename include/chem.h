@@ -167,6 +167,8 @@ typedef struct {
                                    this layout) predicted this call: sum_cells min(hint, actual) /
                                    sum_cells max(hint, actual); -1 without hints.  schedule_lpt = 2
                                    engages heavy-first only while the last value is >= 0.9        */
+    int64_t kernel_launches;    /* kernels this call enqueued (integration, gate, compaction, sort,
+                                   bookkeeping transfers)                                          */
 } chem_stats;
 
 typedef struct chem_ctx chem_ctx;   /* opaque, library-owned */

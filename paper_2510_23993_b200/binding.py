@@ -62,7 +62,7 @@ class ChemStats(ctypes.Structure):
         (n, ctypes.c_double) for n in ("t_gate_ms", "t_bulk_ms", "t_compact_ms", "t_sparse_ms",
                                        "max_energy_drift")] + [("active_per_iter", ctypes.c_int64 * 16)] + [
         (n, ctypes.c_int64) for n in ("warp_substeps", "bulk_substeps", "lockstep", "lpt")] + [
-        ("hint_accuracy", ctypes.c_double)]
+        ("hint_accuracy", ctypes.c_double), ("kernel_launches", ctypes.c_int64)]
 
     def to_dict(self):
         d = {n: getattr(self, n) for n, _ in self._fields_ if n != "active_per_iter"}

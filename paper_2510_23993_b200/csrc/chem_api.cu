@@ -371,6 +371,8 @@ int ensure_host_boxes(chem_ctx* c, int32_t nb)
 // its next command start only when the copy engine is through with every larger copy queued on it by
 // then, so a host-buffer caller that overlaps the D2H of one box group with the next call (HostRunner)
 // saw each call wait for the previous group's whole D2H (tools/e2e_timeline.py, profiles/r02_e2e_timeline_*).
+thread_local int64_t t_launches = 0;   // kernels enqueued by the current call (chem_stats.kernel_launches)
+
 __global__ void k_copy_words(const unsigned long long* __restrict__ src, unsigned long long* __restrict__ dst,
                              int64_t n)
 {
@@ -391,6 +393,7 @@ cudaError_t copy_words(void* dst, const void* src, size_t bytes, cudaStream_t s)
     const int grid = (int)std::min<int64_t>(64, (n + 255) / 256);
     k_copy_words<<<grid, 256, 0, s>>>(static_cast<const unsigned long long*>(src),
                                        static_cast<unsigned long long*>(dst), n);
+    ++t_launches;
     return cudaGetLastError();
 }
 
@@ -399,6 +402,7 @@ cudaError_t zero_bytes(void* dst, size_t bytes, cudaStream_t s)
     if (bytes == 0) return cudaSuccess;
     const int grid = (int)std::min<int64_t>(256, ((int64_t)bytes + 255) / 256);
     k_zero_bytes<<<grid, 256, 0, s>>>(static_cast<unsigned char*>(dst), (int64_t)bytes);
+    ++t_launches;
     return cudaGetLastError();
 }
 
@@ -707,6 +711,7 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
     chem_stats st;
     std::memset(&st, 0, sizeof(st));
     st.cells = total;
+    t_launches = 0;
     cudaError_t e;
 #define CK(x)                                        \
     do {                                             \
@@ -719,6 +724,7 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
     if (box_cost) CK(zero_bytes(box_cost, sizeof(double) * nboxes, s));
     if (total == 0) {
         CK(cudaStreamSynchronize(s));
+        st.kernel_launches = t_launches;
         if (stats) *stats = st;
         return CHEM_OK;
     }
@@ -736,6 +742,7 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
     uint32_t* key0 = reinterpret_cast<uint32_t*>(base + W.key0);
     uint32_t* key1 = reinterpret_cast<uint32_t*>(base + W.key1);
     k_gate<kStreamBS><<<grid_for(total, kStreamBS), kStreamBS, 0, s>>>(L, ids0, key0);
+    ++t_launches;
     CK(cudaGetLastError());
     CK(cudaEventRecord(c->ev[1], s));
     int64_t n_active = 0;
@@ -747,6 +754,7 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
         CK(zero_bytes(c->trace, sizeof(int32_t) * (size_t)c->trace_rows * nboxes, s));
         if (n_active > 0) {
             k_box_count<kStreamBS><<<grid_for(n_active, kStreamBS), kStreamBS, 0, s>>>(L, ids0, n_active, c->trace);
+            ++t_launches;
             CK(cudaGetLastError());
         }
     }
@@ -797,8 +805,11 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
         unsigned* hist = reinterpret_cast<unsigned*>(key1);
         const int ntiles = (int)((n + kSortTile - 1) / kSortTile);
         k_bucket_hist<<<ntiles, kSortBS, 0, s>>>(keys, n, hist, ntiles);
+        ++t_launches;
         k_scan_excl<<<1, 1024, 0, s>>>(hist, (int64_t)ntiles * kCostBuckets);
+        ++t_launches;
         k_bucket_scatter<<<ntiles, kSortBS, 0, s>>>(keys, ids_in, n, hist, ntiles, ids_out);
+        ++t_launches;
         return cudaGetLastError();
     };
     if (lpt) {
@@ -826,6 +837,7 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
         const uint32_t* lst = all_cells ? nullptr : cur;
         const int64_t nl = all_cells ? total : n_cur;
         CK(cudaEventRecord(c->ev[0], s));
+        ++t_launches;
         if (lock)
             CK(ops.integrate_lock(c->params.data(), o.method, L, lst, nl, kmax_b, 0, 0, c->num_sms, s));
         else
@@ -837,6 +849,7 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
         CK(cudaEventRecord(c->ev[0], s));
         CK(zero_bytes(L.stats + S_COUNT_ACTIVE, 8, s));
         k_compact<kStreamBS><<<grid_for(nl, kStreamBS), kStreamBS, 0, s>>>(L, lst, nl, nxt);
+        ++t_launches;
         CK(cudaGetLastError());
         CK(cudaEventRecord(c->ev[1], s));
         CK(read_count(n_cur));
@@ -850,6 +863,7 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
         if (tracing && st.bulk_iters < c->trace_rows && n_cur > 0) {
             k_box_count<kStreamBS><<<grid_for(n_cur, kStreamBS), kStreamBS, 0, s>>>(
                 L, nxt, n_cur, c->trace + (size_t)st.bulk_iters * nboxes);
+            ++t_launches;
             CK(cudaGetLastError());
         }
         cur = nxt;
@@ -860,6 +874,7 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
             // active after the first burst; skewed (max > 1.5 mean) or forced -> sort, one persistent launch
             CK(zero_bytes(L.stats + S_PRED2_TOTAL, 16, s));
             k_predict<kStreamBS><<<grid_for(n_cur, kStreamBS), kStreamBS, 0, s>>>(L, cur, n_cur, key0);
+            ++t_launches;
             CK(cudaGetLastError());
             int64_t dummy;
             CK(read_count(dummy));
@@ -891,18 +906,21 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
             // heavy-first on the previous call's hints: the whole active list, light cells included, as
             // persistent lockstep blocks (one per SM) with lane refill - a free-running refill grid costs
             // 1-substep cells their coalesced loads (cfg5 at the production tolerance 507 vs 345, r02)
+            ++t_launches;
             CK(ops.integrate_lock(c->params.data(), o.method, L, cur, n_cur, o.kmax_sparse, 1, 1, c->num_sms, s));
         } else {
             // the sparse list (after the bursts; sorted heaviest first under the in-call prediction) on
             // the free-running persistent grid with lane refill (lockstep costs 2-7 % here, r02t)
             const int grid = std::max(1, std::min<int>(c->num_sms * ops.blocks_per_sm(o.method),
                                                        (int)((n_cur + kIntegrateBS - 1) / kIntegrateBS)));
+            ++t_launches;
             CK(ops.integrate(c->params.data(), o.method, L, cur, n_cur, o.kmax_sparse, 1, 1, grid, s));
         }
         CK(cudaEventRecord(c->ev[1], s));
     }
     if (box_cost && n_active > 0) {
         k_box_cost<kStreamBS><<<grid_for(n_active, kStreamBS), kStreamBS, 0, s>>>(L, ids0, n_active, box_cost);
+        ++t_launches;
         CK(cudaGetLastError());
     }
     CK(copy_words(c->d_stats, L.stats, S_NSTATS * 8, s));
@@ -922,6 +940,7 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
     st.hint_accuracy = (history && hs[S_HINT_MAX] > 0) ? (double)hs[S_HINT_MIN] / (double)hs[S_HINT_MAX] : -1.0;
     unsigned long long db = hs[S_DRIFT_BITS];
     std::memcpy(&st.max_energy_drift, &db, 8);
+    st.kernel_launches = t_launches;
     if (stats) *stats = st;
 #undef CK
     return CHEM_OK;
