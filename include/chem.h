@@ -18,7 +18,10 @@
  *  - Layout is component-major ("column-major", Alg. 1): component c of cell i
  *    is at p[c*ld + i], ld >= n.  Species order is the mechanism's.
  *  - SI units: rho kg/m^3, e J/kg (mass-specific internal energy), T K, t s, Omega mol/(m^3 s).
- *  - All device work is enqueued on `stream` (a cudaStream_t, NULL = legacy default stream).
+ *  - All device work is enqueued on `stream` (a cudaStream_t, NULL = legacy default stream), as
+ *    kernels only: the library's own small transfers (box table in, counters out) go through mapped
+ *    pinned memory, never through a copy engine, so a caller's large copies on other streams do not
+ *    hold back its next command.
  *  - Return 0 on success or a negative CHEM_E* code; text via chem_strerror().  Per-cell
  *    problems (non-convergence, non-finite state) are NOT call errors: they are counted in
  *    chem_stats.  The library never aborts the process.
