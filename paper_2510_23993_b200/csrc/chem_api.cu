@@ -371,6 +371,9 @@ int ensure_host_boxes(chem_ctx* c, int32_t nb)
 // its next command start only when the copy engine is through with every larger copy queued on it by
 // then, so a host-buffer caller that overlaps the D2H of one box group with the next call (HostRunner)
 // saw each call wait for the previous group's whole D2H (tools/e2e_timeline.py, profiles/r02_e2e_timeline_*).
+// lane-refill batch of the sparse launch (k_integrate's `refill`): cost-sorted list / gate-ordered list
+constexpr int kRefillSorted = 1, kRefillUnsorted = 8;
+
 thread_local int64_t t_launches = 0;   // kernels enqueued by the current call (chem_stats.kernel_launches)
 
 __global__ void k_copy_words(const unsigned long long* __restrict__ src, unsigned long long* __restrict__ dst,
@@ -907,14 +910,16 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
             // persistent lockstep blocks (one per SM) with lane refill - a free-running refill grid costs
             // 1-substep cells their coalesced loads (cfg5 at the production tolerance 507 vs 345, r02)
             ++t_launches;
-            CK(ops.integrate_lock(c->params.data(), o.method, L, cur, n_cur, o.kmax_sparse, 1, 1, c->num_sms, s));
+            CK(ops.integrate_lock(c->params.data(), o.method, L, cur, n_cur, o.kmax_sparse, kRefillSorted, 1,
+                                  c->num_sms, s));
         } else {
             // the sparse list (after the bursts; sorted heaviest first under the in-call prediction) on
             // the free-running persistent grid with lane refill (lockstep costs 2-7 % here, r02t)
             const int grid = std::max(1, std::min<int>(c->num_sms * ops.blocks_per_sm(o.method),
                                                        (int)((n_cur + kIntegrateBS - 1) / kIntegrateBS)));
             ++t_launches;
-            CK(ops.integrate(c->params.data(), o.method, L, cur, n_cur, o.kmax_sparse, 1, 1, grid, s));
+            CK(ops.integrate(c->params.data(), o.method, L, cur, n_cur, o.kmax_sparse,
+                             lpt ? kRefillSorted : kRefillUnsorted, 1, grid, s));
         }
         CK(cudaEventRecord(c->ev[1], s));
     }

@@ -335,14 +335,6 @@ __global__ void __launch_bounds__(BS) k_box_count(LaunchCtx L, const uint32_t* i
 }
 
 // ----------------------------------------------------------------------------- A6/A7/A9 integrate
-// persistent lane refill: idle lanes of a warp with busy lanes wait until this many are idle (round 1
-// batched 8; on the cost-sorted lists of round 2 refilling every idle lane at once is fastest: cfg3
-// 195.8 -> 200.7, cfg5 279.2 -> 294.3 Mcell-steps/s, batches of 2 / 4 in between, r02v)
-#ifdef CHEM_REFILL_BATCH
-constexpr int kRefillBatch = CHEM_REFILL_BATCH;
-#else
-constexpr int kRefillBatch = 1;
-#endif
 // Per-thread shared memory (stride = block size, conflict-free): the n x n iteration matrix
 // (I/(h gamma) - J, then its LU) and the stored stage vectors K_s (pivot rows stay in registers);
 // n = NSA+1 unknowns (reacting Y_k and T, Eq. 6).  Stiffly accurate methods (RODAS4) do not store
@@ -760,9 +752,14 @@ __device__ __forceinline__ void flush_counters(const LaunchCtx& L, Counters& c)
     if ((threadIdx.x & 31) == 0 && bits) atomicMax(&L.stats[S_DRIFT_BITS], bits);
 }
 
-// Bulk (refill = false): thread i takes ids[i] (identity when ids == nullptr, the paper's
-// all-cells launch) and runs <= kmax attempted substeps.  Sparse (refill = true): persistent
-// grid; each lane pulls ids from the atomic cursor S_CURSOR until the list is exhausted.
+// Bulk (refill = 0): thread i takes ids[i] (identity when ids == nullptr, the paper's
+// all-cells launch) and runs <= kmax attempted substeps.  Sparse (refill = b >= 1): persistent
+// grid; each lane pulls ids from the atomic cursor S_CURSOR until the list is exhausted, the idle
+// lanes of a warp that still has busy lanes waiting until b of them are idle (the host passes 1 for a
+// cost-sorted list, where neighbouring entries cost alike and refilling at once is fastest — cfg3 195.8
+// -> 200.7, cfg5 279.2 -> 294.3 Mcell-steps/s against b = 8, r02v — and a quarter warp for the
+// gate-ordered list of Alg. 3, where joint loads of a batch win: sparse-only cfg3 61 (b = 1) vs 92, r02
+// NEXT-2 sweeps).
 // Both modes run the same substep code, so results are bitwise independent of K_max and N*.
 // LOCK: the block's warps take each substep together (one __syncthreads_or per substep), so that on a
 // heterogeneous field the SM's resident warps stay in the same code region (shared instruction cache)
@@ -836,7 +833,7 @@ __global__ void __launch_bounds__(BS) k_integrate(const __grid_constant__ Params
                 const unsigned need = __ballot_sync(FULL, !have && live);
                 if (need == 0) break;
                 const unsigned busy = __ballot_sync(FULL, have);
-                if (busy != 0 && __popc(need) < kRefillBatch) break;
+                if (busy != 0 && __popc(need) < refill) break;
                 const int leader = __ffs(need) - 1;
                 unsigned long long base = 0;
                 if (lane == leader) base = atomicAdd(&L.stats[S_CURSOR], (unsigned long long)__popc(need));
