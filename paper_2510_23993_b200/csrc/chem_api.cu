@@ -1,6 +1,7 @@
 // chem_api.cu — the C ABI of include/chem.h: validation, structure matching, workspace, and the
 // host side of the bulk-sparse schedule (Alg. 3).
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: phase ranges for nsys / ncu --nvtx (no cost unattached)
 
 #include <algorithm>
 #include <cmath>
@@ -374,6 +375,12 @@ int ensure_host_boxes(chem_ctx* c, int32_t nb)
 // lane-refill batch of the sparse launch (k_integrate's `refill`): cost-sorted list / gate-ordered list
 constexpr int kRefillSorted = 1, kRefillUnsorted = 8;
 
+// NVTX range for one scope (the call and its Alg. 3 phases show up by name on a profiler timeline)
+struct NvtxScope {
+    explicit NvtxScope(const char* name) { nvtxRangePushA(name); }
+    ~NvtxScope() { nvtxRangePop(); }
+};
+
 thread_local int64_t t_launches = 0;   // kernels enqueued by the current call (chem_stats.kernel_launches)
 
 __global__ void k_copy_words(const unsigned long long* __restrict__ src, unsigned long long* __restrict__ dst,
@@ -653,6 +660,7 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
                          size_t ws_bytes, double* box_cost, chem_stats* stats, void* stream)
 {
     CHEM_PRE(c);
+    NvtxScope nvtx_call("chem_integrate_boxes");
     if (nboxes < 1 || !boxes || !(rtol > 0.0) || !(atol > 0.0) || !ws) return CHEM_EINVAL;
     int64_t total = 0;
     for (int b = 0; b < nboxes; ++b) {
@@ -741,6 +749,7 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
     };
 
     // ---- Alg. 3 §1: gate + count + index map
+    nvtxMarkA("chem: gate");
     CK(cudaEventRecord(c->ev[0], s));
     uint32_t* key0 = reinterpret_cast<uint32_t*>(base + W.key0);
     uint32_t* key1 = reinterpret_cast<uint32_t*>(base + W.key1);
@@ -823,6 +832,7 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
     }
 
     // ---- Alg. 3 §2: bulk bursts while N_active > N*
+    nvtxMarkA("chem: bulk");
     // lockstep bursts (chem_opts.lockstep; auto: the previous call's bulk SIMT efficiency was low)
     const bool lock = o.method != CHEM_METHOD_EXPLICIT &&
                       (o.lockstep == 1 || (o.lockstep == 2 && c->simt_eff < kLockEff));
@@ -901,6 +911,7 @@ int chem_integrate_boxes(chem_ctx* c, int32_t nboxes, const chem_box* boxes, dou
     }
 
     // ---- Alg. 3 §3: sparse integration over the index map (persistent, lane refill)
+    nvtxMarkA("chem: sparse");
     st.sparse_cells = n_cur;
     if (n_cur > 0) {
         CK(zero_bytes(L.stats + S_CURSOR, 8, s));
