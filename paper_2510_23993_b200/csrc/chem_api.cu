@@ -366,12 +366,6 @@ int ensure_host_boxes(chem_ctx* c, int32_t nb)
     return CHEM_OK;
 }
 
-// The call's bookkeeping transfers (box table in, counters out; a few hundred bytes to ~100 KB) and its
-// small memsets run as kernels on the caller's stream, through the mapped buffers above, never as
-// copy-engine operations: a stream whose previous command was a cudaMemcpyAsync / cudaMemsetAsync lets
-// its next command start only when the copy engine is through with every larger copy queued on it by
-// then, so a host-buffer caller that overlaps the D2H of one box group with the next call (HostRunner)
-// saw each call wait for the previous group's whole D2H (tools/e2e_timeline.py, profiles/r02_e2e_timeline_*).
 // lane-refill batch of the sparse launch (k_integrate's `refill`): cost-sorted list / gate-ordered list
 constexpr int kRefillSorted = 1, kRefillUnsorted = 8;
 
@@ -383,6 +377,12 @@ struct NvtxScope {
 
 thread_local int64_t t_launches = 0;   // kernels enqueued by the current call (chem_stats.kernel_launches)
 
+// The call's bookkeeping transfers (box table in, counters out; a few hundred bytes to ~100 KB) and its
+// small memsets run as kernels on the caller's stream, through the mapped buffers above, never as
+// copy-engine operations: a stream whose previous command was a cudaMemcpyAsync / cudaMemsetAsync lets
+// its next command start only when the copy engine is through with every larger copy queued on it by
+// then, so a host-buffer caller that overlaps the D2H of one box group with the next call (HostRunner)
+// saw each call wait for the previous group's whole D2H (tools/e2e_timeline.py, profiles/r02_e2e_timeline_*).
 __global__ void k_copy_words(const unsigned long long* __restrict__ src, unsigned long long* __restrict__ dst,
                              int64_t n)
 {
