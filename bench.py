@@ -794,6 +794,11 @@ def ours(args):
                        "k_integrate_ms": res["k_ms"] / args.steps,
                        "integrate_launches": launches_int, "substeps_per_cell_step": att / max(wl_cs, 1),
                        "accepted_per_cell_step": acc / max(wl_cs, 1),
+                       # SURVEY §8(d) "also reported" rates, this rank's calls over the (max-over-ranks) step time
+                       "rates_per_s": {k: sum(s[f] for s in stats) / (res["ms_per_step"] * args.steps * 1e-3)
+                                       for k, f in (("active_cell_steps", "active0"),
+                                                    ("substeps_attempted", "steps_attempted"),
+                                                    ("rhs_evals", "rhs_evals"))},
                        "frozen_per_cell_step": sum(s.get("steps_frozen", 0) for s in stats) / args.steps
                        / max(wl_cs, 1), "bulk_iters": s0["bulk_iters"],
                        "active_per_iter": s0["active_per_iter"], "sparse_cells": s0["sparse_cells"],
