@@ -398,6 +398,16 @@ def host_info():
     return dict(cpu_model=model or platform.processor(), smt=smt, nproc=os.cpu_count())
 
 
+def host_threads(o):
+    """Threads for the oracle baseline: every host core this process may run on.  torchrun exports
+    OMP_NUM_THREADS=1 to its ranks, which would time the reference arm / cpu_baseline on one core."""
+    try:
+        n = len(os.sched_getaffinity(0))
+    except AttributeError:
+        n = os.cpu_count() or 1
+    return max(n, o.max_threads())
+
+
 def oracle_sample(meta, seconds_target, rtol, atol):
     """Time the oracle, as it stands, on a bounded sample of the workload's cells (all host cores)."""
     from oracle import Oracle
@@ -405,7 +415,7 @@ def oracle_sample(meta, seconds_target, rtol, atol):
     st = meta["state"]
     Y = np.asarray(st["Y"])
     e = o.energy(st["T"], Y)
-    nth = o.max_threads()
+    nth = host_threads(o)
 
     def run(n, threads=nth):
         t0 = time.perf_counter()
@@ -510,7 +520,7 @@ def oracle_stratified(chem, wl, rtol, atol, seconds_target, n_prop=65536, n_heav
         e = np.array([o.energy(t, y) for t, y in zip(T, Y)])    # the oracle's own thermo
         return rho, e, T, Y, dt
 
-    nth = o.max_threads()
+    nth = host_threads(o)
 
     def run(data, threads):
         rho, e, T, Y, dt = data
