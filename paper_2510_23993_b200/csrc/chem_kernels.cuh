@@ -415,12 +415,10 @@ __device__ __forceinline__ int ros_step(const Params<M>& P, const LaunchCtx& L, 
     if (h >= remaining) { h = remaining; last = true; }
     if (!(h > 4.0 * 2.220446049250313e-16 * C.dt) || !isfinite(h)) return -1;  // step-size underflow
 
-    // iteration matrix A = I/(h gamma) - J, LU in place
+    // iteration matrix A = I/(h gamma) - J, LU in place (rhs_jac left -J in A)
     const double ghinv = 1.0 / (h * Meth::gamma);
 #pragma unroll
-    for (int i = 0; i < n; ++i)
-#pragma unroll
-        for (int j = 0; j < n; ++j) A(i, j) = (i == j) ? ghinv - A(i, j) : -A(i, j);
+    for (int i = 0; i < n; ++i) A(i, i) = ghinv + A(i, i);
     uint64_t perm;
     const bool ok = lu_factor<n>(A, perm);
 
