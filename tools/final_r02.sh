@@ -23,8 +23,10 @@ for c in cfg2 cfg3 cfg4 cfg5; do
 done
 ncu --set full --clock-control none --import-source on -k regex:k_integrate -c 1 -f -o gpurun_out/${T}_cfg2 \
     python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --also none --no-schedules --no-prod > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:k_integrate --launch-skip 3 -c 1 -f -o gpurun_out/${T}_cfg3lpt \
-    python bench.py --config cfg3 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --also none --no-schedules --no-prod > /dev/null 2>&1
+# the timed call's two k_integrate launches (first lockstep burst + heavy-first persistent launch) after 3 warm-up
+# calls (launches per call: 2, 1 on the cross-call hints of the second call, 2, 2)
+ncu --set full --clock-control none --import-source on -k regex:k_integrate --launch-skip 5 -c 2 -f -o gpurun_out/${T}_cfg3lpt \
+    python bench.py --config cfg3 --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --also none --no-schedules --no-prod > /dev/null 2>&1
 python tools/ncu_summary.py gpurun_out/${T}_cfg2.ncu-rep > gpurun_out/${T}_ncu_cfg2.txt 2>&1
 python tools/ncu_summary.py gpurun_out/${T}_cfg3lpt.ncu-rep > gpurun_out/${T}_ncu_cfg3lpt.txt 2>&1
 head -14 gpurun_out/${T}_ncu_cfg2.txt; head -6 gpurun_out/${T}_ncu_cfg3lpt.txt
