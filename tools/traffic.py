@@ -28,9 +28,10 @@ def main(tag, *cfgs):
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
         tot = sum(v["dram__bytes_read.sum"] * scale[unit["dram__bytes_read.sum"]] +
                   v["dram__bytes_write.sum"] * scale[unit["dram__bytes_write.sum"]] for v in ks)
+        keep = {k: v for k, v in doc.get(c, {}).items() if k.startswith("ncu_")}   # FP64-pipe % from full captures
         doc[c] = {"traffic_bytes_per_launch": tot / max(len(ks), 1), "launches": len(ks),
                   "source": f"ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum over every k_integrate "
-                            f"launch of `bench.py --config {c} --steps 1 --warmup 3` (gpurun {tag})"}
+                            f"launch of `bench.py --config {c} --steps 1 --warmup 3` (gpurun {tag})", **keep}
         print(c, doc[c])
     json.dump(doc, open(path, "w"), indent=1)
 
